@@ -1,0 +1,303 @@
+#!/usr/bin/env python
+"""Benchmark of the presorted-DP placement hot path (Heddle, §5.2).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Workload (BASELINE.json configs[3], the metric's batched sweep): 16384 independent
+placement problems, n = 1024 sorted predicted trajectory lengths into m = 32
+workers with random sorted MP degrees over {1,2,4,8}, FP32 costs, Eq. 3 min-max.
+A step = one pass of the whole hot path over the batch: validation + cost tables +
+every DP layer (heddle_place_solve) and the backtrack (heddle_place_backtrack).
+With N GPUs (torchrun, one process per GPU) the 16384 problems are block-sharded
+across ranks with no collective (strong scaling: fixed total work).
+
+value = DP cells/s = (problems x W(n, m)) / device time, W = the (state, split)
+transitions of Eq. 3 (include/heddle_place.h).  `--impl reference` times the CPU
+oracle (oracle/) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "placement-DP cells/s and solves/s at 1/2/4/8 B200; % of HBM/ALU roofline"
+B_TOTAL, N, M = 16384, 1024, 32
+WORKLOAD = ("batched sweep (BASELINE configs[3]): 16384 independent N=1024 K=32 placement problems, "
+            "coding(Pareto)/search(log-normal) families alternating, predicted FP32 lengths, random sorted "
+            "MP degrees over {1,2,4,8}, Eq. 3 min-max")
+SM_COUNT = 148
+ISSUE_SLOTS_PER_CELL = 3   # FMUL + FMNMX(max) + FMNMX(min); measured issue rates in profiles/r01_alu_peaks.jsonl
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def alu_peak_cells(sm_mhz):
+    """Issue-bound peak of the exhaustive Eq. 3 reduction: 4 SMSPs x 1 warp-instr/clk x 32 lanes
+    / 3 instructions per transition, x 148 SMs x clock."""
+    return SM_COUNT * 4 * 32 / ISSUE_SLOTS_PER_CELL * sm_mhz * 1e6
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    def __init__(self, dev_index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+            "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+            "hw_power_brake_slowdown": 0x80, "display_clock_setting": 0x100}
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit and k != "gpu_idle":
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            self._stop.wait(0.05)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def shard(B, world, rank):
+    lo = rank * B // world
+    hi = (rank + 1) * B // world
+    return lo, hi
+
+
+# ------------------------------------------------------------------------------ oracle arm
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle
+    from inputs import workloads as wl
+    from paper_2603_28101_b200 import _lib
+    oracle.build()
+    threads = os.cpu_count() or 1
+    sample = args.ref_sample
+    batch = wl.config_batched()
+    W = _lib.transitions(N, M)
+    times = []
+    for step in range(args.warmup + args.steps):
+        lo = (step * sample) % batch.B
+        idx = np.arange(lo, lo + sample) % batch.B
+        rws = np.stack([batch.profile.row_of(batch.degrees[b]) for b in idx])
+        t = time.perf_counter()
+        oracle.solve_batch(batch.lengths[idx], batch.profile.T, batch.profile.F, rws, mode="f32", threads=threads)
+        dt = time.perf_counter() - t
+        if step >= args.warmup:
+            times.append(dt)
+    tot = sum(times)
+    value = sample * W * len(times) / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "problems": B_TOTAL, "n": N, "m": M, "semiring": "minmax",
+                   "parallelism": "host OpenMP over problems"},
+        "solves_per_s": sample * len(times) / tot,
+        "cpu_baseline": {"value": value, "unit": "cells/s", "cores": threads, "kind": "oracle",
+                         "sample": f"{sample} problems of the batched sweep per step (FP32-emulating FP64 oracle, "
+                                   f"plain O(n^2 m) DP with back-pointers)"},
+        "e2e": {"value": value, "unit": "cells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(sample=64):
+    """The oracle as it stands, on a bounded sample of the workload, on all host cores."""
+    import oracle
+    from inputs import workloads as wl
+    from paper_2603_28101_b200 import _lib
+    oracle.build()
+    threads = os.cpu_count() or 1
+    batch = wl.config_batched(B=sample, seed_problem=1)
+    rws = np.stack([batch.profile.row_of(batch.degrees[b]) for b in range(sample)])
+    t = time.perf_counter()
+    _, _, used = oracle.solve_batch(batch.lengths, batch.profile.T, batch.profile.F, rws, mode="f32", threads=threads)
+    dt = time.perf_counter() - t
+    return {"value": sample * _lib.transitions(N, M) / dt, "unit": "cells/s", "cores": used, "kind": "oracle",
+            "sample": f"{sample} problems (n={N}, m={M}) of the batched-sweep workload, {dt:.1f} s wall"}
+
+
+# ------------------------------------------------------------------------------ CUDA arm
+def run_cuda(args):
+    import torch
+    import torch.distributed as dist
+
+    from inputs import workloads as wl
+    from paper_2603_28101_b200 import _lib
+    from paper_2603_28101_b200.placer import Placer
+
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    lo, hi = shard(B_TOTAL, world, rank)
+    Bl = hi - lo
+    batch = wl.config_batched()
+    L = torch.from_numpy(np.ascontiguousarray(batch.lengths[lo:hi])).to(dev)
+    D = torch.from_numpy(np.ascontiguousarray(batch.degrees[lo:hi].astype(np.int32))).to(dev)
+    Lh = torch.from_numpy(np.ascontiguousarray(batch.lengths[lo:hi])).pin_memory()
+    Dh = torch.from_numpy(np.ascontiguousarray(batch.degrees[lo:hi].astype(np.int32))).pin_memory()
+    placer = Placer.from_profile(batch.profile, max_n=N, max_m=M, max_batch=Bl, device=local)
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
+
+    def step():
+        placer.solve(L, D)
+        placer.backtrack()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    launches0 = placer.launches
+    with ClockSampler(local) as clk:
+        for s in range(args.steps):
+            flush.fill_(float(s))                      # L2 flush between timed iterations (not timed)
+            ev[s][0].record(stream)
+            placer.solve(L, D)
+            ev[s][1].record(stream)
+            placer.backtrack()
+            ev[s][2].record(stream)
+        torch.cuda.synchronize()
+    launches = placer.launches - launches0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_step = sum(e[0].elapsed_time(e[2]) for e in ev) / 1e3          # seconds, K steps
+    t_k2 = sum(e[0].elapsed_time(e[1]) for e in ev) / 1e3            # dominant kernel: K2 solve
+    W = _lib.transitions(N, M)
+
+    # end to end through the public API with host buffers (H2D + solve + backtrack + D2H each step)
+    for _ in range(2):
+        placer.solve_host(Lh, Dh)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    h2d = d2h = 0
+    for s in range(args.steps):
+        _, _, _, h2d, d2h = placer.solve_host(Lh, Dh)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t_e2e = e0.elapsed_time(e1) / 1e3
+
+    vals = torch.tensor([t_step, t_k2, t_e2e, float(launches)], dtype=torch.float64, device=dev)
+    if world > 1:
+        mx = vals.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = vals.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        t_step, t_k2, t_e2e = mx[0].item(), mx[1].item(), mx[2].item()
+        launches = int(sm[3].item())
+    cells = B_TOTAL * W * args.steps
+    if rank == 0:
+        value = cells / t_step
+        clocks = clk.summary()
+        pk = peaks()
+        peak_mhz = pk.get("sm_max_mhz", 1965.0)
+        k2_rate = Bl * W * args.steps / t_k2        # per GPU, the dominant kernel alone
+        peak = alu_peak_cells(peak_mhz)
+        line = {
+            "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * t_step / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "problems": B_TOTAL, "n": N, "m": M, "semiring": "minmax",
+                       "transitions_per_problem": W, "parallelism": f"dp{world} (problems block-sharded, no collective)",
+                       "l2": "flushed between timed steps (256 MiB device write, untimed)"},
+            "solves_per_s": B_TOTAL * args.steps / t_step,
+            "roofline": {"bound": "alu", "achieved": k2_rate / 1e9, "peak": peak / 1e9, "unit": "Gcell/s",
+                         "frac": k2_rate / peak, "traffic": args.traffic,
+                         "kernel": "k2_dp_batched<F32,MINMAX>",
+                         "peak_basis": f"148 SMs x 4 SMSP x 32 lanes / 3 issue slots per cell x {peak_mhz:.0f} MHz "
+                                       "(measured issue rates, profiles/r01_alu_peaks.jsonl)",
+                         "kernel_share_of_step": t_k2 / t_step},
+            "e2e": {"value": cells / t_e2e, "unit": "cells/s", "h2d_bytes_per_step": h2d * world,
+                    "d2h_bytes_per_step": d2h * world},
+            "gpu_launches": launches,
+            "clocks": clocks,
+        }
+        if not args.no_cpu_baseline and world == 1:
+            line["cpu_baseline"] = cpu_baseline(args.cpu_sample)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=64)
+    ap.add_argument("--ref-sample", type=int, default=32)
+    ap.add_argument("--traffic", type=float, default=None, help="ncu dram bytes per K2 launch (from profiles/)")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        import __graft_entry__
+        __graft_entry__.build()
+        run_cuda(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,165 @@
+/*
+ * heddle_place.h -- C ABI of the B200-native presorted-DP trajectory placement
+ * (Heddle, arxiv 2603.28101, §5.2 "Presorted Dynamic Programming").
+ *
+ * Citations: "P:n" = PAPER.md line n (section / equation named alongside),
+ * "S:n" = SPEC.md line n.  The meaning of every argument follows the paper's
+ * problem statement (§5.1): n trajectories with lengths L sorted in
+ * descending order, m rollout workers, a base per-token time T and an
+ * interference factor F that depends only on the group size, per worker
+ * MP degree (§6.1, sorted mapping P:703-706).
+ *
+ * What one solve computes, per problem (Eq. 3, stored as dp[j][i]):
+ *     dp[0][0] = 0
+ *     dp[j][i] = min_{k in [j-1, i-1]}  dp[j-1][k]  (+)  L[k] * G_j(i - k)
+ *     G_j(s)   = T[d_j] * F[d_j][min(s, s_max) - 1]
+ *     (+) = max (HEDDLE_MINMAX, Eq. 3, default) or + (HEDDLE_MINPLUS)
+ *     cost  = +inf when the group exceeds the worker's cap (size > caps[j]) or
+ *             its token sum Sp[i] - Sp[k] exceeds kv_caps[j]  (R6)
+ *     back-pointer parent[j][i] = the LOWEST k attaining the minimum (R3)
+ *     objective = dp[m][n] = the Eq. 2 makespan of the optimal
+ *     contiguous partition (Lemma 1);  boundaries
+ *     b_m = n,  b_{j-1} = parent[j][b_j],  0 = b_0 < b_1 < ... < b_m = n.
+ * Only states on a complete m-group partition are computed: i in [j, n-m+j].
+ *
+ * Arithmetic per dtype (R7):
+ *   HEDDLE_F32: G = fl32(T*F) (float32 T, F), cost = fl32(L*G); MINPLUS
+ *               v = fmaf(L, G, dp).  MINMAX values are selections => exact
+ *               w.r.t. the float32 emulation; <= 2^-23 relative vs FP64.
+ *   HEDDLE_F64: G = T*F, cost = L*G, MINPLUS v = fma(L, G, dp), all double.
+ *   HEDDLE_U32: integer profile; G = T*F exactly (must be < 2^32); cost =
+ *               L*G exactly; MINMAX objective uint32, MINPLUS objective uint64.
+ *               Range guard: max L * max G < 2^32 - 65536 and L <= 65535,
+ *               else the problem reports HEDDLE_E_RANGE (never a silent wrap).
+ *
+ * Memory / ownership: every pointer in heddle_place_problem and every output
+ * pointer is a DEVICE pointer owned by the caller, borrowed for the
+ * stream-ordered duration of the call; the caller keeps problem buffers alive
+ * until heddle_place_backtrack() of the same solve has been enqueued and the
+ * stream has passed it.  Host pointers appear only in heddle_place_config
+ * (copied at init) and in heddle_place_solve_host() (copied inside the call).
+ * The context owns its device workspace (dp rows, status words, cost tables),
+ * sized at init from max_n / max_m / max_batch.
+ *
+ * Errors: every call returns a heddle_status and never aborts, throws or exits.
+ * Argument errors are detected on the host before anything is enqueued, and
+ * then nothing is written.  Per-problem data errors (unsorted lengths, NaN,
+ * unknown degree, range) and infeasibility are detected ON THE DEVICE and
+ * reported per problem in status_out[b] (heddle_status values); such a
+ * problem's objective is the dtype's +inf / UINT max and its boundaries are -1.
+ * solve / backtrack are asynchronous on `stream` (a cudaStream_t, NULL = the
+ * legacy default stream).  A context is not thread-safe; distinct contexts are
+ * independent.
+ */
+#ifndef HEDDLE_PLACE_H
+#define HEDDLE_PLACE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HEDDLE_OK = 0,
+  HEDDLE_E_INVALID = 1,        /* null pointer, n<1, m<1, B<1, sizes above the ctx limits, bad enum */
+  HEDDLE_E_UNSORTED = 2,       /* lengths not non-increasing or degrees not non-increasing */
+  HEDDLE_E_INFEASIBLE = 3,     /* n < m or capacities cannot cover the n trajectories        */
+  HEDDLE_E_RANGE = 4,          /* NaN/inf/<=0 length or profile value, F decreasing, U32 guard */
+  HEDDLE_E_UNKNOWN_DEGREE = 5, /* a worker's MP degree is not in the profile                   */
+  HEDDLE_E_STATE = 6,          /* backtrack before solve, parents requested without KEEP_PARENTS      */
+  HEDDLE_E_CUDA = 7,           /* a CUDA runtime call failed                                          */
+  HEDDLE_E_NCCL = 8,           /* an NCCL call failed (split mode)                                    */
+  HEDDLE_E_NOMEM = 9           /* device or host allocation failed                                    */
+} heddle_status;
+
+typedef enum { HEDDLE_U32 = 0, HEDDLE_F32 = 1, HEDDLE_F64 = 2 } heddle_dtype;
+typedef enum { HEDDLE_MINMAX = 0 /* Eq. 3, default */, HEDDLE_MINPLUS = 1 } heddle_semiring;
+
+/* config.flags */
+#define HEDDLE_KEEP_PARENTS 0x1u  /* solve records every back-pointer (slower inner loop) */
+
+typedef struct heddle_place_ctx heddle_place_ctx;
+
+/* Interference profile and workspace limits.  Host memory,
+ * copied at init.  Element type of T and F: float (F32), double (F64), uint32 (U32). */
+typedef struct {
+  int32_t device;          /* CUDA device ordinal                                          */
+  int32_t dtype;           /* heddle_dtype                                                 */
+  int32_t semiring;        /* heddle_semiring                                              */
+  int32_t max_n;           /* largest n a solve may use (>= 1)                             */
+  int32_t max_m;           /* largest m (>= 1)                                             */
+  int32_t max_batch;       /* largest B (>= 1)                                             */
+  int32_t num_degrees;     /* D >= 1 rows in the profile                                   */
+  const int32_t* degrees;  /* [D] distinct MP degrees (e.g. {1,2,4,8}), > 0                 */
+  const void* T;           /* [D] base per-token time at batch size 1, > 0          */
+  const void* F;           /* [D][s_max] interference factor for batch size 1..s_max,      */
+                           /*   > 0 and non-decreasing in the size; clamped beyond */
+  int32_t s_max;           /* profiled range, >= 1                            */
+  uint32_t flags;          /* HEDDLE_KEEP_PARENTS                                          */
+} heddle_place_config;
+
+/* A uniform-shape batch of B independent placement problems.  Device memory.
+ * A stride is the element distance between consecutive problems' rows; stride
+ * 0 broadcasts one row to all problems (e.g. one L swept over TP degrees). */
+typedef struct {
+  int32_t n;                    /* trajectories per problem, 1 <= n <= max_n                    */
+  int32_t m;                    /* workers per problem, 1 <= m <= max_m  (n < m => INFEASIBLE)  */
+  int32_t B;                    /* problems, 1 <= B <= max_batch                               */
+  const void* lengths;          /* [B][n] dtype: predicted length L, non-increasing    */
+  int64_t lengths_stride;
+  const int32_t* degrees;       /* [B][m] MP degree of worker j, non-increasing    */
+  int64_t degrees_stride;
+  const int32_t* caps;          /* [B][m] max trajectories per worker, <0 = unbounded; or NULL  */
+  int64_t caps_stride;
+  const int64_t* kv_caps;       /* [B][m] max group token sum, <0 = unbounded; or NULL          */
+  int64_t kv_caps_stride;
+} heddle_place_problem;
+
+/* Creates a context on cfg->device: copies and validates the profile (E_RANGE
+ * if T/F are not positive/finite, F decreases, or a U32 product T*F >= 2^32),
+ * builds the per-degree cost tables G_d[s] on the device (cost-table kernel),
+ * and allocates the workspace.  *out is NULL on failure. */
+heddle_status heddle_place_init(const heddle_place_config* cfg, heddle_place_ctx** out);
+
+/* Enqueues the DP for all B problems on `stream`.
+ *   objective_out : device [B]; float (F32), double (F64), uint32 (U32 MINMAX),
+ *                   uint64 (U32 MINPLUS).  dp[m][n] of each problem.
+ *   status_out    : device int32 [B] per-problem heddle_status, or NULL.
+ * The context remembers the problem descriptor for heddle_place_backtrack(). */
+heddle_status heddle_place_solve(heddle_place_ctx* ctx, const heddle_place_problem* prob,
+                                 void* objective_out, int32_t* status_out, void* stream);
+
+/* Enqueues the backtrack of the last solve.
+ *   boundaries_out : device int32 [B][m+1], b_0 = 0 < ... < b_m = n (or -1s).
+ *   parents_out    : device int32 [B][m][n+1] or NULL.  Row j-1 holds
+ *                    parent[j][i] for i in [j, n-m+j] and -1 elsewhere.
+ *                    Requires HEDDLE_KEEP_PARENTS (else E_STATE). */
+heddle_status heddle_place_backtrack(heddle_place_ctx* ctx, int32_t* boundaries_out,
+                                     int32_t* parents_out, void* stream);
+
+/* End-to-end convenience with HOST buffers: copies the problem arrays (host
+ * pointers, same layout as heddle_place_problem) to the device, solves,
+ * backtracks, copies objective / boundaries / status back to host memory and
+ * synchronises `stream`.  Pinned host memory makes the copies asynchronous.
+ * bytes_h2d / bytes_d2h (may be NULL) receive the bytes copied each way. */
+heddle_status heddle_place_solve_host(heddle_place_ctx* ctx, const heddle_place_problem* host_prob,
+                                      void* objective_host, int32_t* boundaries_host,
+                                      int32_t* status_host, void* stream,
+                                      int64_t* bytes_h2d, int64_t* bytes_d2h);
+
+/* Number of kernels this context has launched since init (for bench evidence). */
+int64_t heddle_place_launch_count(const heddle_place_ctx* ctx);
+
+/* Algorithmic transitions W(n, m) of one problem: the (state, split) pairs the
+ * DP evaluates on the computed region:
+ * W = 2(n-m+1) + (m-2)(n-m+1)(n-m+2)/2 for m >= 2, W(n,1) = 1, 0 if n < m. */
+int64_t heddle_place_transitions(int32_t n, int32_t m);
+
+void heddle_place_destroy(heddle_place_ctx* ctx);
+const char* heddle_place_strerror(heddle_status s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HEDDLE_PLACE_H */

@@ -1,0 +1,95 @@
+"""ctypes binding of include/heddle_place.h -- argument marshalling only.
+
+Every step of the placement DP runs in the CUDA kernels of libheddle_place.so;
+this module only turns torch tensors into device pointers and streams.  There
+is no CPU fallback: importing it without the built library raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libheddle_place.so")
+
+OK, E_INVALID, E_UNSORTED, E_INFEASIBLE, E_RANGE, E_UNKNOWN_DEGREE, E_STATE, E_CUDA, E_NCCL, E_NOMEM = range(10)
+U32, F32, F64 = 0, 1, 2
+MINMAX, MINPLUS = 0, 1
+KEEP_PARENTS = 0x1
+
+DTYPES = {"u32": U32, "f32": F32, "f64": F64}
+SEMIRINGS = {"minmax": MINMAX, "minplus": MINPLUS}
+
+# exported symbols declared in include/heddle_place.h (tests check the .so exports all of them)
+SYMBOLS = ("heddle_place_init", "heddle_place_solve", "heddle_place_backtrack", "heddle_place_solve_host",
+           "heddle_place_launch_count", "heddle_place_transitions", "heddle_place_destroy",
+           "heddle_place_strerror")
+
+
+class Config(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int32), ("dtype", ctypes.c_int32), ("semiring", ctypes.c_int32),
+                ("max_n", ctypes.c_int32), ("max_m", ctypes.c_int32), ("max_batch", ctypes.c_int32),
+                ("num_degrees", ctypes.c_int32), ("degrees", ctypes.c_void_p),
+                ("T", ctypes.c_void_p), ("F", ctypes.c_void_p), ("s_max", ctypes.c_int32),
+                ("flags", ctypes.c_uint32)]
+
+
+class Problem(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("m", ctypes.c_int32), ("B", ctypes.c_int32),
+                ("lengths", ctypes.c_void_p), ("lengths_stride", ctypes.c_int64),
+                ("degrees", ctypes.c_void_p), ("degrees_stride", ctypes.c_int64),
+                ("caps", ctypes.c_void_p), ("caps_stride", ctypes.c_int64),
+                ("kv_caps", ctypes.c_void_p), ("kv_caps_stride", ctypes.c_int64)]
+
+
+class HeddleError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        self.status = status
+        super().__init__(f"{what}: {strerror(status)} ({status})")
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libheddle_place.so (built in-tree by __graft_entry__.build())."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                              "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        vp = ctypes.c_void_p
+        L.heddle_place_init.argtypes = [ctypes.POINTER(Config), ctypes.POINTER(vp)]
+        L.heddle_place_init.restype = ctypes.c_int
+        L.heddle_place_solve.argtypes = [vp, ctypes.POINTER(Problem), vp, vp, vp]
+        L.heddle_place_solve.restype = ctypes.c_int
+        L.heddle_place_backtrack.argtypes = [vp, vp, vp, vp]
+        L.heddle_place_backtrack.restype = ctypes.c_int
+        L.heddle_place_solve_host.argtypes = [vp, ctypes.POINTER(Problem), vp, vp, vp, vp,
+                                              ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
+        L.heddle_place_solve_host.restype = ctypes.c_int
+        L.heddle_place_launch_count.argtypes = [vp]
+        L.heddle_place_launch_count.restype = ctypes.c_int64
+        L.heddle_place_transitions.argtypes = [ctypes.c_int32, ctypes.c_int32]
+        L.heddle_place_transitions.restype = ctypes.c_int64
+        L.heddle_place_destroy.argtypes = [vp]
+        L.heddle_place_destroy.restype = None
+        L.heddle_place_strerror.argtypes = [ctypes.c_int]
+        L.heddle_place_strerror.restype = ctypes.c_char_p
+        _lib = L
+    return _lib
+
+
+def strerror(status: int) -> str:
+    return lib().heddle_place_strerror(status).decode()
+
+
+def transitions(n: int, m: int) -> int:
+    """W(n, m): algorithmic transitions of one problem (the DP-cell unit of the metric)."""
+    return int(lib().heddle_place_transitions(n, m))
+
+
+def check(status: int, what: str):
+    if status != OK:
+        raise HeddleError(status, what)

@@ -1,0 +1,76 @@
+// K4 -- backtrack ("identifies the optimal partition index k").
+//
+// b_m = n;  b_{j-1} = parent[j][b_j] = the LOWEST k in [j-1, b_j - 1] with
+//     dp[j-1][k] (+) L[k] * G_j(b_j - k) == dp[j][b_j]
+// recomputed from the stored dp rows with the exact arithmetic of the DP kernel
+// (Tr<>::comb), so the result is bit-identical to a stored argmin table.
+// One warp per problem: 32 splits per step, __ballot_sync + __ffs picks the
+// lowest matching k; O(m * n / 32) per problem against the DP's O(n^2 m).
+#pragma once
+#include "dp_batched.cuh"
+
+namespace hp {
+
+constexpr int kK4Warps = 8;
+
+template <int DT, int SR, bool KV>
+__global__ void __launch_bounds__(32 * kK4Warps) k4_backtrack(SolveArgs a, int32_t* bounds) {
+  using T = Tr<DT, SR>;
+  using L = typename T::L;
+  using G = typename T::G;
+  using D = typename T::D;
+  using S = typename SpT<DT>::type;
+  const int lane = threadIdx.x & 31;
+  const int b = blockIdx.x * kK4Warps + (threadIdx.x >> 5);
+  if (b >= a.B) return;
+  const int n = a.n, m = a.m;
+  int32_t* out = bounds + (int64_t)b * (m + 1);
+  if (a.status[b] != HEDDLE_OK) {
+    for (int j = lane; j <= m; j += 32) out[j] = -1;
+    return;
+  }
+  const L* gL = reinterpret_cast<const L*>(a.lengths) + (int64_t)b * a.ls;
+  const D* gdp = reinterpret_cast<const D*>(a.dpws) + (int64_t)b * (m + 1) * (n + 1);
+  const G* gtab = reinterpret_cast<const G*>(a.gtab);
+  const S* gSp = KV ? reinterpret_cast<const S*>(a.spws) + (int64_t)b * (n + 1) : nullptr;
+  int cur = n;
+  if (lane == 0) out[m] = n;
+  for (int j = m; j >= 2; --j) {
+    const D target = gdp[(int64_t)j * (n + 1) + cur];
+    const int d = a.degrees[(int64_t)b * a.ds + j - 1];
+    int row = 0;
+    for (int q = 0; q < a.D; ++q) row = (a.prof_deg[q] == d) ? q : row;
+    const G* grow = gtab + (int64_t)row * a.gstride;
+    int lo = j - 1;
+    const int cap = a.caps ? a.caps[(int64_t)b * a.cs + j - 1] : -1;
+    if (cap >= 0) lo = max(lo, cur - cap);
+    if constexpr (KV) {
+      const int64_t kvc = a.kv[(int64_t)b * a.kvs + j - 1];
+      if (kvc >= 0) {
+        int l = lo, h = cur;   // smallest k with Sp[cur] - Sp[k] <= kv (monotone in k)
+        while (l < h) {
+          int mid = (l + h) >> 1;
+          if (gSp[cur] - gSp[mid] <= (S)kvc) h = mid; else l = mid + 1;
+        }
+        lo = l;
+      }
+    }
+    int found = -1;
+    for (int base = lo; base < cur && found < 0; base += 32) {
+      const int k = base + lane;
+      bool hit = false;
+      if (k < cur) hit = (T::norm(T::comb(gdp[(int64_t)(j - 1) * (n + 1) + k], gL[k], grow[cur - k])) == target);
+      const unsigned msk = __ballot_sync(0xffffffffu, hit);
+      if (msk) found = base + __ffs(msk) - 1;
+    }
+    if (found < 0) {   // unreachable: the target is one of these candidates
+      for (int q = lane; q <= m; q += 32) out[q] = -1;
+      return;
+    }
+    cur = found;
+    if (lane == 0) out[j - 1] = cur;
+  }
+  if (lane == 0) out[0] = 0;
+}
+
+}  // namespace hp

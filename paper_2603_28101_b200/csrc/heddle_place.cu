@@ -1,0 +1,404 @@
+// C-ABI of the B200-native presorted-DP placement (include/heddle_place.h).
+// Host side: argument validation, profile validation, workspace, kernel
+// dispatch.  Device side: K1 cost tables (this file), K2 batched DP
+// (dp_batched.cuh), K4 backtrack (backtrack.cuh).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "backtrack.cuh"
+#include "dp_batched.cuh"
+#include "heddle_place.h"
+
+using namespace hp;
+
+// ------------------------------------------------------------------------ K1
+// Cost tables G_d[s] = T_d * F_d(min(s, s_max)) for s = 1..max_n (
+// clamp S:90).  Entry 0 is never read.  F32: fl32(T*F); F64: T*F; U32: exact.
+template <int DT>
+__global__ void k1_cost_tables(const void* T, const void* F, int D, int s_max, int gstride, void* gtab) {
+  const int d = blockIdx.y;
+  for (int s = 1 + blockIdx.x * blockDim.x + threadIdx.x; s < gstride; s += gridDim.x * blockDim.x) {
+    const int f = (s < s_max ? s : s_max) - 1;
+    if constexpr (DT == HEDDLE_F32) {
+      reinterpret_cast<float*>(gtab)[(int64_t)d * gstride + s] =
+          __fmul_rn(reinterpret_cast<const float*>(T)[d], reinterpret_cast<const float*>(F)[(int64_t)d * s_max + f]);
+    } else if constexpr (DT == HEDDLE_F64) {
+      reinterpret_cast<double*>(gtab)[(int64_t)d * gstride + s] =
+          __dmul_rn(reinterpret_cast<const double*>(T)[d], reinterpret_cast<const double*>(F)[(int64_t)d * s_max + f]);
+    } else {
+      reinterpret_cast<uint32_t*>(gtab)[(int64_t)d * gstride + s] =
+          reinterpret_cast<const uint32_t*>(T)[d] * reinterpret_cast<const uint32_t*>(F)[(int64_t)d * s_max + f];
+    }
+  }
+}
+
+// ------------------------------------------------------------------------ context
+struct heddle_place_ctx {
+  int device = 0, dtype = 0, semiring = 0;
+  int max_n = 0, max_m = 0, max_batch = 0, D = 0, s_max = 0;
+  uint32_t flags = 0;
+  int gstride = 0;
+  uint32_t lmax_u32 = 0;
+  void* d_gtab = nullptr;
+  int32_t* d_prof_deg = nullptr;
+  void* d_dp = nullptr;
+  int32_t* d_par = nullptr;
+  void* d_sp = nullptr;
+  int32_t* d_status = nullptr;
+  void* d_stage = nullptr;
+  size_t stage_bytes = 0;
+  bool solved = false;
+  bool last_kv = false;
+  SolveArgs last{};
+  int64_t launches = 0;
+  int smem_optin = 0;
+};
+
+namespace {
+
+size_t elem_size(int dtype) { return dtype == HEDDLE_F64 ? 8 : 4; }
+size_t dp_elem_size(int dtype, int semiring) {
+  return (dtype == HEDDLE_F64 || (dtype == HEDDLE_U32 && semiring == HEDDLE_MINPLUS)) ? 8 : 4;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+using K2Fn = void (*)(SolveArgs);
+using K4Fn = void (*)(SolveArgs, int32_t*);
+
+template <int DT, int SR>
+K2Fn pick_k2(bool kp, bool kv) {
+  if (kp) return kv ? k2_dp_batched<DT, SR, true, true> : k2_dp_batched<DT, SR, true, false>;
+  return kv ? k2_dp_batched<DT, SR, false, true> : k2_dp_batched<DT, SR, false, false>;
+}
+template <int DT, int SR>
+K4Fn pick_k4(bool kv) {
+  return kv ? k4_backtrack<DT, SR, true> : k4_backtrack<DT, SR, false>;
+}
+
+K2Fn k2_for(int dt, int sr, bool kp, bool kv) {
+  if (dt == HEDDLE_F32) return sr == HEDDLE_MINMAX ? pick_k2<HEDDLE_F32, HEDDLE_MINMAX>(kp, kv) : pick_k2<HEDDLE_F32, HEDDLE_MINPLUS>(kp, kv);
+  if (dt == HEDDLE_F64) return sr == HEDDLE_MINMAX ? pick_k2<HEDDLE_F64, HEDDLE_MINMAX>(kp, kv) : pick_k2<HEDDLE_F64, HEDDLE_MINPLUS>(kp, kv);
+  return sr == HEDDLE_MINMAX ? pick_k2<HEDDLE_U32, HEDDLE_MINMAX>(kp, kv) : pick_k2<HEDDLE_U32, HEDDLE_MINPLUS>(kp, kv);
+}
+K4Fn k4_for(int dt, int sr, bool kv) {
+  if (dt == HEDDLE_F32) return sr == HEDDLE_MINMAX ? pick_k4<HEDDLE_F32, HEDDLE_MINMAX>(kv) : pick_k4<HEDDLE_F32, HEDDLE_MINPLUS>(kv);
+  if (dt == HEDDLE_F64) return sr == HEDDLE_MINMAX ? pick_k4<HEDDLE_F64, HEDDLE_MINMAX>(kv) : pick_k4<HEDDLE_F64, HEDDLE_MINPLUS>(kv);
+  return sr == HEDDLE_MINMAX ? pick_k4<HEDDLE_U32, HEDDLE_MINMAX>(kv) : pick_k4<HEDDLE_U32, HEDDLE_MINPLUS>(kv);
+}
+
+int k2_smem(int dt, int sr, int n, int m, bool kv) {
+  if (dt == HEDDLE_F32) return sr == HEDDLE_MINMAX ? K2Smem<HEDDLE_F32, HEDDLE_MINMAX>(n, m, kv).total : K2Smem<HEDDLE_F32, HEDDLE_MINPLUS>(n, m, kv).total;
+  if (dt == HEDDLE_F64) return sr == HEDDLE_MINMAX ? K2Smem<HEDDLE_F64, HEDDLE_MINMAX>(n, m, kv).total : K2Smem<HEDDLE_F64, HEDDLE_MINPLUS>(n, m, kv).total;
+  return sr == HEDDLE_MINMAX ? K2Smem<HEDDLE_U32, HEDDLE_MINMAX>(n, m, kv).total : K2Smem<HEDDLE_U32, HEDDLE_MINPLUS>(n, m, kv).total;
+}
+
+template <class V>
+bool check_profile(const heddle_place_config* c, double* gmax) {
+  const V* T = static_cast<const V*>(c->T);
+  const V* F = static_cast<const V*>(c->F);
+  *gmax = 0;
+  for (int d = 0; d < c->num_degrees; ++d) {
+    const double t = (double)T[d];
+    if (!(t > 0) || !std::isfinite(t)) return false;
+    for (int s = 0; s < c->s_max; ++s) {
+      const double f = (double)F[(int64_t)d * c->s_max + s];
+      if (!(f > 0) || !std::isfinite(f)) return false;
+      if (s > 0 && f < (double)F[(int64_t)d * c->s_max + s - 1]) return false;   // premise P:560
+    }
+    const double g = t * (double)F[(int64_t)d * c->s_max + c->s_max - 1];
+    if (g > *gmax) *gmax = g;
+  }
+  return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* heddle_place_strerror(heddle_status s) {
+  switch (s) {
+    case HEDDLE_OK: return "ok";
+    case HEDDLE_E_INVALID: return "invalid argument";
+    case HEDDLE_E_UNSORTED: return "lengths or degrees not sorted non-increasing";
+    case HEDDLE_E_INFEASIBLE: return "infeasible (n < m or capacities cannot cover n)";
+    case HEDDLE_E_RANGE: return "value out of range (NaN/inf/<=0, F decreasing, or U32 overflow guard)";
+    case HEDDLE_E_UNKNOWN_DEGREE: return "MP degree not in the profile";
+    case HEDDLE_E_STATE: return "bad call order or missing HEDDLE_KEEP_PARENTS";
+    case HEDDLE_E_CUDA: return "CUDA error";
+    case HEDDLE_E_NCCL: return "NCCL error";
+    case HEDDLE_E_NOMEM: return "out of memory";
+  }
+  return "unknown status";
+}
+
+int64_t heddle_place_transitions(int32_t n, int32_t m) {
+  if (n < 1 || m < 1 || n < m) return 0;
+  if (m == 1) return 1;
+  const int64_t w = (int64_t)n - m + 1;
+  return 2 * w + (int64_t)(m - 2) * w * (w + 1) / 2;
+}
+
+int64_t heddle_place_launch_count(const heddle_place_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+void heddle_place_destroy(heddle_place_ctx* ctx) {
+  if (!ctx) return;
+  DeviceGuard g(ctx->device);
+  cudaFree(ctx->d_gtab);
+  cudaFree(ctx->d_prof_deg);
+  cudaFree(ctx->d_dp);
+  cudaFree(ctx->d_par);
+  cudaFree(ctx->d_sp);
+  cudaFree(ctx->d_status);
+  cudaFree(ctx->d_stage);
+  delete ctx;
+}
+
+heddle_status heddle_place_init(const heddle_place_config* c, heddle_place_ctx** out) {
+  if (!out) return HEDDLE_E_INVALID;
+  *out = nullptr;
+  if (!c || !c->degrees || !c->T || !c->F) return HEDDLE_E_INVALID;
+  if (c->dtype < HEDDLE_U32 || c->dtype > HEDDLE_F64) return HEDDLE_E_INVALID;
+  if (c->semiring != HEDDLE_MINMAX && c->semiring != HEDDLE_MINPLUS) return HEDDLE_E_INVALID;
+  if (c->max_n < 1 || c->max_m < 1 || c->max_batch < 1 || c->num_degrees < 1 || c->s_max < 1) return HEDDLE_E_INVALID;
+  if (c->max_n > (1 << 24)) return HEDDLE_E_INVALID;
+  for (int d = 0; d < c->num_degrees; ++d) {
+    if (c->degrees[d] <= 0) return HEDDLE_E_INVALID;
+    for (int e = 0; e < d; ++e)
+      if (c->degrees[e] == c->degrees[d]) return HEDDLE_E_INVALID;
+  }
+  double gmax = 0;
+  uint32_t lmax = 0;
+  if (c->dtype == HEDDLE_F32) {
+    if (!check_profile<float>(c, &gmax)) return HEDDLE_E_RANGE;
+  } else if (c->dtype == HEDDLE_F64) {
+    if (!check_profile<double>(c, &gmax)) return HEDDLE_E_RANGE;
+  } else {
+    if (!check_profile<uint32_t>(c, &gmax)) return HEDDLE_E_RANGE;
+    const uint32_t* T = static_cast<const uint32_t*>(c->T);
+    const uint32_t* F = static_cast<const uint32_t*>(c->F);
+    uint64_t g64 = 0;
+    for (int d = 0; d < c->num_degrees; ++d) {
+      const uint64_t g = (uint64_t)T[d] * (uint64_t)F[(int64_t)d * c->s_max + c->s_max - 1];
+      if (g > g64) g64 = g;
+    }
+    if (g64 >= (uint64_t)kU32Thresh) return HEDDLE_E_RANGE;
+    // every admissible cost L*G must stay below 2^32 - 65536 and L <= 65535 (traits.cuh)
+    const uint64_t lim = ((uint64_t)kU32Thresh - 1) / g64;
+    lmax = (uint32_t)(lim < 65535 ? lim : 65535);
+    if (lmax < 1) return HEDDLE_E_RANGE;
+  }
+
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || c->device < 0 || c->device >= ndev) return HEDDLE_E_CUDA;
+  DeviceGuard guard(c->device);
+  heddle_place_ctx* x = new (std::nothrow) heddle_place_ctx();
+  if (!x) return HEDDLE_E_NOMEM;
+  x->device = c->device;
+  x->dtype = c->dtype;
+  x->semiring = c->semiring;
+  x->max_n = c->max_n;
+  x->max_m = c->max_m;
+  x->max_batch = c->max_batch;
+  x->D = c->num_degrees;
+  x->s_max = c->s_max;
+  x->flags = c->flags;
+  x->gstride = c->max_n + 1;
+  x->lmax_u32 = lmax;
+  cudaDeviceGetAttribute(&x->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device);
+
+  const size_t es = elem_size(c->dtype);
+  const size_t des = dp_elem_size(c->dtype, c->semiring);
+  const size_t cells = (size_t)c->max_batch * (size_t)(c->max_m + 1) * (size_t)(c->max_n + 1);
+  void *dT = nullptr, *dF = nullptr;
+  bool ok = cudaMalloc(&x->d_gtab, es * (size_t)x->D * x->gstride) == cudaSuccess &&
+            cudaMalloc(&x->d_prof_deg, 4 * (size_t)x->D) == cudaSuccess &&
+            cudaMalloc(&x->d_dp, des * cells) == cudaSuccess &&
+            cudaMalloc(&x->d_sp, 8 * (size_t)c->max_batch * (size_t)(c->max_n + 1)) == cudaSuccess &&
+            cudaMalloc(&x->d_status, 4 * (size_t)c->max_batch) == cudaSuccess &&
+            cudaMalloc(&dT, es * (size_t)x->D) == cudaSuccess &&
+            cudaMalloc(&dF, es * (size_t)x->D * c->s_max) == cudaSuccess;
+  if (ok && (c->flags & HEDDLE_KEEP_PARENTS)) ok = cudaMalloc(&x->d_par, 4 * cells) == cudaSuccess;
+  if (!ok) {
+    cudaGetLastError();
+    cudaFree(dT);
+    cudaFree(dF);
+    heddle_place_destroy(x);
+    return HEDDLE_E_NOMEM;
+  }
+  ok = cudaMemcpy(x->d_prof_deg, c->degrees, 4 * (size_t)x->D, cudaMemcpyHostToDevice) == cudaSuccess &&
+       cudaMemcpy(dT, c->T, es * (size_t)x->D, cudaMemcpyHostToDevice) == cudaSuccess &&
+       cudaMemcpy(dF, c->F, es * (size_t)x->D * c->s_max, cudaMemcpyHostToDevice) == cudaSuccess;
+  if (ok) {
+    dim3 grid((x->gstride + 255) / 256, x->D);
+    if (c->dtype == HEDDLE_F32) k1_cost_tables<HEDDLE_F32><<<grid, 256>>>(dT, dF, x->D, c->s_max, x->gstride, x->d_gtab);
+    else if (c->dtype == HEDDLE_F64) k1_cost_tables<HEDDLE_F64><<<grid, 256>>>(dT, dF, x->D, c->s_max, x->gstride, x->d_gtab);
+    else k1_cost_tables<HEDDLE_U32><<<grid, 256>>>(dT, dF, x->D, c->s_max, x->gstride, x->d_gtab);
+    x->launches++;
+    ok = cudaGetLastError() == cudaSuccess && cudaDeviceSynchronize() == cudaSuccess;
+  }
+  cudaFree(dT);
+  cudaFree(dF);
+  if (!ok) {
+    heddle_place_destroy(x);
+    return HEDDLE_E_CUDA;
+  }
+  // opt in to large dynamic shared memory for every K2 variant this ctx may launch
+  for (int kp = 0; kp < 2; ++kp)
+    for (int kv = 0; kv < 2; ++kv)
+      cudaFuncSetAttribute(k2_for(x->dtype, x->semiring, kp, kv), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           x->smem_optin);
+  cudaGetLastError();
+  *out = x;
+  return HEDDLE_OK;
+}
+
+heddle_status heddle_place_solve(heddle_place_ctx* x, const heddle_place_problem* p, void* objective_out,
+                                 int32_t* status_out, void* stream) {
+  if (!x || !p || !objective_out || !p->lengths || !p->degrees) return HEDDLE_E_INVALID;
+  if (p->n < 1 || p->m < 1 || p->B < 1 || p->n > x->max_n || p->m > x->max_m || p->B > x->max_batch)
+    return HEDDLE_E_INVALID;
+  if (p->lengths_stride < 0 || p->degrees_stride < 0 || p->caps_stride < 0 || p->kv_caps_stride < 0)
+    return HEDDLE_E_INVALID;
+  const bool kv = p->kv_caps != nullptr;
+  const bool kp = (x->flags & HEDDLE_KEEP_PARENTS) != 0;
+  const int smem = k2_smem(x->dtype, x->semiring, p->n, p->m, kv);
+  if (smem > x->smem_optin) return HEDDLE_E_INVALID;   // n too large for the one-CTA-per-problem kernel
+  DeviceGuard guard(x->device);
+  SolveArgs a{};
+  a.n = p->n;
+  a.m = p->m;
+  a.B = p->B;
+  a.lengths = p->lengths;
+  a.ls = p->lengths_stride;
+  a.degrees = p->degrees;
+  a.ds = p->degrees_stride;
+  a.caps = p->caps;
+  a.cs = p->caps_stride;
+  a.kv = p->kv_caps;
+  a.kvs = p->kv_caps_stride;
+  a.gtab = x->d_gtab;
+  a.gstride = x->gstride;
+  a.prof_deg = x->d_prof_deg;
+  a.D = x->D;
+  a.lmax_u32 = x->lmax_u32;
+  a.dpws = x->d_dp;
+  a.parws = x->d_par;
+  a.spws = x->d_sp;
+  a.status = x->d_status;
+  a.status_out = status_out;
+  a.objective = objective_out;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  k2_for(x->dtype, x->semiring, kp, kv)<<<p->B, kK2Threads, smem, s>>>(a);
+  x->launches++;
+  if (cudaGetLastError() != cudaSuccess) return HEDDLE_E_CUDA;
+  x->last = a;
+  x->last_kv = kv;
+  x->solved = true;
+  return HEDDLE_OK;
+}
+
+heddle_status heddle_place_backtrack(heddle_place_ctx* x, int32_t* boundaries_out, int32_t* parents_out,
+                                     void* stream) {
+  if (!x || !boundaries_out) return HEDDLE_E_INVALID;
+  if (!x->solved) return HEDDLE_E_STATE;
+  if (parents_out && !(x->flags & HEDDLE_KEEP_PARENTS)) return HEDDLE_E_STATE;
+  DeviceGuard guard(x->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const SolveArgs& a = x->last;
+  k4_for(x->dtype, x->semiring, x->last_kv)<<<(a.B + kK4Warps - 1) / kK4Warps, 32 * kK4Warps, 0, s>>>(a, boundaries_out);
+  x->launches++;
+  if (cudaGetLastError() != cudaSuccess) return HEDDLE_E_CUDA;
+  if (parents_out) {
+    const size_t row = 4 * (size_t)(a.n + 1);
+    if (cudaMemcpy2DAsync(parents_out, row * a.m, x->d_par + (size_t)(a.n + 1), row * (a.m + 1), row * a.m, a.B,
+                          cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+      return HEDDLE_E_CUDA;
+  }
+  return HEDDLE_OK;
+}
+
+heddle_status heddle_place_solve_host(heddle_place_ctx* x, const heddle_place_problem* hp_, void* objective_host,
+                                      int32_t* boundaries_host, int32_t* status_host, void* stream,
+                                      int64_t* bytes_h2d, int64_t* bytes_d2h) {
+  if (!x || !hp_ || !objective_host || !boundaries_host || !hp_->lengths || !hp_->degrees) return HEDDLE_E_INVALID;
+  const heddle_place_problem& p = *hp_;
+  if (p.n < 1 || p.m < 1 || p.B < 1 || p.n > x->max_n || p.m > x->max_m || p.B > x->max_batch)
+    return HEDDLE_E_INVALID;
+  DeviceGuard guard(x->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t es = elem_size(x->dtype);
+  const size_t oes = dp_elem_size(x->dtype, x->semiring);
+  const int64_t B = p.B, n = p.n, m = p.m;
+  const int64_t lrows = p.lengths_stride == 0 ? 1 : B;
+  const int64_t drows = p.degrees_stride == 0 ? 1 : B;
+  const int64_t crows = p.caps ? (p.caps_stride == 0 ? 1 : B) : 0;
+  const int64_t krows = p.kv_caps ? (p.kv_caps_stride == 0 ? 1 : B) : 0;
+  auto al = [](size_t v) { return (v + 255) & ~(size_t)255; };
+  const size_t bl = al(es * lrows * n), bd = al(4 * drows * m), bc = al(4 * crows * m), bk = al(8 * krows * m);
+  const size_t bo = al(8 * B), bb = al(4 * B * (m + 1)), bs = al(4 * B);
+  const size_t need = bl + bd + bc + bk + bo + bb + bs;
+  if (need > x->stage_bytes) {
+    cudaFree(x->d_stage);
+    x->d_stage = nullptr;
+    x->stage_bytes = 0;
+    if (cudaMalloc(&x->d_stage, need) != cudaSuccess) { cudaGetLastError(); return HEDDLE_E_NOMEM; }
+    x->stage_bytes = need;
+  }
+  char* base = static_cast<char*>(x->d_stage);
+  char *dl = base, *dd = dl + bl, *dc = dd + bd, *dk = dc + bc, *dob = dk + bk, *dbd = dob + bo, *dst = dbd + bb;
+  int64_t h2d = 0, d2h = 0;
+  auto up = [&](void* dst_, const void* src, int64_t rows, int64_t cols, int64_t stride, size_t esz) -> bool {
+    if (rows == 0) return true;
+    const size_t w = esz * cols;
+    h2d += (int64_t)(w * rows);
+    if (stride == cols || rows == 1)
+      return cudaMemcpyAsync(dst_, src, w * rows, cudaMemcpyHostToDevice, s) == cudaSuccess;
+    return cudaMemcpy2DAsync(dst_, w, src, esz * stride, w, rows, cudaMemcpyHostToDevice, s) == cudaSuccess;
+  };
+  if (!up(dl, p.lengths, lrows, n, p.lengths_stride, es) || !up(dd, p.degrees, drows, m, p.degrees_stride, 4) ||
+      !up(dc, p.caps, crows, m, p.caps_stride, 4) || !up(dk, p.kv_caps, krows, m, p.kv_caps_stride, 8))
+    return HEDDLE_E_CUDA;
+  heddle_place_problem q = p;
+  q.lengths = dl;
+  q.lengths_stride = p.lengths_stride == 0 ? 0 : n;
+  q.degrees = reinterpret_cast<const int32_t*>(dd);
+  q.degrees_stride = p.degrees_stride == 0 ? 0 : m;
+  q.caps = p.caps ? reinterpret_cast<const int32_t*>(dc) : nullptr;
+  q.caps_stride = p.caps_stride == 0 ? 0 : m;
+  q.kv_caps = p.kv_caps ? reinterpret_cast<const int64_t*>(dk) : nullptr;
+  q.kv_caps_stride = p.kv_caps_stride == 0 ? 0 : m;
+  heddle_status st = heddle_place_solve(x, &q, dob, reinterpret_cast<int32_t*>(dst), stream);
+  if (st != HEDDLE_OK) return st;
+  st = heddle_place_backtrack(x, reinterpret_cast<int32_t*>(dbd), nullptr, stream);
+  if (st != HEDDLE_OK) return st;
+  bool ok = cudaMemcpyAsync(objective_host, dob, oes * B, cudaMemcpyDeviceToHost, s) == cudaSuccess &&
+            cudaMemcpyAsync(boundaries_host, dbd, 4 * B * (m + 1), cudaMemcpyDeviceToHost, s) == cudaSuccess;
+  d2h += (int64_t)(oes * B + 4 * B * (m + 1));
+  if (ok && status_host) {
+    ok = cudaMemcpyAsync(status_host, dst, 4 * B, cudaMemcpyDeviceToHost, s) == cudaSuccess;
+    d2h += 4 * B;
+  }
+  if (!ok || cudaStreamSynchronize(s) != cudaSuccess) return HEDDLE_E_CUDA;
+  if (bytes_h2d) *bytes_h2d = h2d;
+  if (bytes_d2h) *bytes_d2h = d2h;
+  return HEDDLE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,231 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Inputs are the seeded synthetic workloads of inputs/workloads.py, at the
+BASELINE.json configs (tiny, rollout, TP sweep, batched sweep) and in the
+bench.py launch configuration; see tests/parity.py for the acceptance rule.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from inputs import workloads as wl
+from tests.parity import assert_exact, assert_f64_tolerance, run_gpu, to_dev
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _build():
+    import __graft_entry__
+    __graft_entry__.build()
+
+
+# ------------------------------------------------------------------ configs[0]: tiny, integer, brute force
+@pytest.mark.parametrize("semiring", ["minmax", "minplus"])
+def test_tiny_config_bruteforce(semiring):
+    for prob in range(8):
+        batch = wl.config_tiny(problem=prob)
+        gpu = run_gpu(batch, semiring=semiring, keep_parents=True)
+        p = oracle.Problem.from_batch(batch, 0, mode="u32",
+                                      semiring=oracle.MINMAX if semiring == "minmax" else oracle.MINPLUS)
+        ref = oracle.solve(p, want_tables=True)
+        assert_exact(gpu, 0, ref, batch, "u32", semiring, check_parents=True, tag=f"tiny{prob}")
+        bf = oracle.brute_contiguous(p)
+        assert gpu["obj"][0] == bf["opt"]
+        cp = oracle.canonical_parents_bf(p)
+        n, m = batch.n, batch.m
+        for j in range(2, m):
+            got = gpu["parents"][0][j - 1, j:n - m + j + 1]
+            assert np.array_equal(got, cp["parent"][j, j:n - m + j + 1]), (prob, j)
+
+
+@pytest.mark.parametrize("semiring", ["minmax", "minplus"])
+@pytest.mark.parametrize("dtype", ["u32", "f32"])
+def test_random_tiny_exact(dtype, semiring):
+    """Heavy ties, clamp plateaus, caps, kv caps, heterogeneous degrees: bit-exact."""
+    sr = oracle.MINMAX if semiring == "minmax" else oracle.MINPLUS
+    for s in range(150):
+        batch = wl.tiny_random(s, n_max=20, m_max=6, allow_caps=True, allow_kv=True, dtype=dtype)
+        gpu = run_gpu(batch, semiring=semiring, keep_parents=(s % 2 == 0))
+        ref = oracle.solve(oracle.Problem.from_batch(batch, 0, mode=dtype, semiring=sr), want_tables=True)
+        assert_exact(gpu, 0, ref, batch, dtype, semiring, check_parents=(s % 2 == 0), tag=f"{dtype}{s}")
+        gpu["placer"].close()
+
+
+@pytest.mark.parametrize("semiring", ["minmax", "minplus"])
+def test_random_tiny_f64(semiring):
+    sr = oracle.MINMAX if semiring == "minmax" else oracle.MINPLUS
+    for s in range(80):
+        batch = wl.tiny_random(s, n_max=20, m_max=6, allow_caps=True, allow_kv=True, dtype="f64")
+        gpu = run_gpu(batch, semiring=semiring)
+        p = oracle.Problem.from_batch(batch, 0, mode="f64", semiring=sr)
+        ref = oracle.solve(p)
+        if ref["status"] != oracle.OK:
+            assert gpu["status"][0] == ref["status"]
+            continue
+        assert gpu["status"][0] == 0
+        assert_f64_tolerance(gpu["obj"][0], gpu["bounds"][0], p, semiring, tag=f"f64-{s}")
+        gpu["placer"].close()
+
+
+# ------------------------------------------------------------------ configs[1]: rollout, FP32
+@pytest.mark.parametrize("semiring", ["minmax", "minplus"])
+def test_rollout_config(semiring):
+    sr = oracle.MINMAX if semiring == "minmax" else oracle.MINPLUS
+    for prob in range(4):
+        batch = wl.config_rollout(problem=prob)
+        gpu = run_gpu(batch, semiring=semiring, keep_parents=True)
+        ref = oracle.solve(oracle.Problem.from_batch(batch, 0, mode="f32", semiring=sr), want_tables=True)
+        assert_exact(gpu, 0, ref, batch, "f32", semiring, check_parents=True, tag=f"rollout{prob}")
+        p64 = oracle.Problem.from_batch(batch, 0, mode="f64", semiring=sr)
+        assert_f64_tolerance(gpu["obj"][0], gpu["bounds"][0], p64, semiring, tag=f"rollout{prob}")
+
+
+def test_rollout_with_caps_and_kv():
+    """Worker batch caps (max_active) and KV token caps on the rollout workload."""
+    batch = wl.config_rollout(problem=7)
+    rng = np.random.default_rng(11)
+    batch.caps = rng.integers(16, 40, size=(1, batch.m)).astype(np.int32)
+    total = float(batch.lengths.astype(np.float64).sum())
+    batch.kv_caps = rng.integers(int(total / 20), int(total / 8), size=(1, batch.m)).astype(np.int64)
+    gpu = run_gpu(batch, keep_parents=True)
+    ref = oracle.solve(oracle.Problem.from_batch(batch, 0, mode="f32"), want_tables=True)
+    assert_exact(gpu, 0, ref, batch, "f32", "minmax", check_parents=True, tag="rollout-caps")
+
+
+# ------------------------------------------------------------------ configs[2]: TP sweep (shared L, stride 0)
+def test_tp_sweep_config():
+    batch = wl.config_tp_sweep()
+    gpu = run_gpu(batch, lengths_shared=True)
+    rows = np.stack([batch.profile.row_of(batch.degrees[b]) for b in range(batch.B)])
+    opt, bounds, _ = oracle.solve_batch(batch.lengths, batch.profile.T, batch.profile.F, rows, mode="f32")
+    for b in range(batch.B):
+        assert gpu["status"][b] == 0
+        assert gpu["obj"][b] == opt[b], (b, gpu["obj"][b], opt[b])
+        assert np.array_equal(gpu["bounds"][b], bounds[b]), b
+
+
+# ------------------------------------------------------------------ configs[3]: batched sweep
+def test_batched_sample_exact():
+    batch = wl.config_batched(B=96)
+    gpu = run_gpu(batch)
+    rows = np.stack([batch.profile.row_of(batch.degrees[b]) for b in range(batch.B)])
+    opt, bounds, _ = oracle.solve_batch(batch.lengths, batch.profile.T, batch.profile.F, rows, mode="f32")
+    assert np.all(gpu["status"] == 0)
+    assert np.array_equal(gpu["obj"], opt)
+    assert np.array_equal(gpu["bounds"], bounds)
+
+
+def test_batched_keep_parents():
+    batch = wl.config_batched(B=6, seed_problem=3)
+    gpu = run_gpu(batch, keep_parents=True)
+    for b in range(batch.B):
+        ref = oracle.solve(oracle.Problem.from_batch(batch, b, mode="f32"), want_tables=True)
+        assert_exact(gpu, b, ref, batch, "f32", "minmax", check_parents=True, tag=f"batched{b}")
+
+
+def test_batched_full_launch_sampled():
+    """The bench.py launch configuration (B=16384, n=1024, m=32), checked on sampled problems."""
+    batch = wl.config_batched()
+    gpu = run_gpu(batch)
+    assert np.all(gpu["status"] == 0)
+    idx = np.random.default_rng(5).choice(batch.B, size=24, replace=False)
+    idx = np.concatenate([idx, [0, 1, batch.B - 1]])
+    rows = np.stack([batch.profile.row_of(batch.degrees[b]) for b in idx])
+    opt, bounds, _ = oracle.solve_batch(batch.lengths[idx], batch.profile.T, batch.profile.F, rows, mode="f32")
+    assert np.array_equal(gpu["obj"][idx], opt)
+    assert np.array_equal(gpu["bounds"][idx], bounds)
+    # property at every size: boundaries strictly increasing from 0 to n
+    bd = gpu["bounds"]
+    assert np.all(bd[:, 0] == 0) and np.all(bd[:, -1] == batch.n) and np.all(np.diff(bd, axis=1) > 0)
+
+
+# ------------------------------------------------------------------ edge cases
+def _single(L, deg, dtype="f32", m=None, profile=None, caps=None, semiring="minmax"):
+    prof = profile or (wl.float_profile() if dtype != "u32" else wl.int_profile())
+    Ln = np.asarray(L)[None, :]
+    b = wl.Batch("edge", Ln.shape[1], len(deg), Ln, np.asarray(deg, dtype=np.int32)[None, :], prof,
+                 caps=None if caps is None else np.asarray(caps, dtype=np.int32)[None, :])
+    return b
+
+
+def test_edge_cases():
+    f = np.float32
+    # n = m = 1
+    g = run_gpu(_single(np.array([100], f), [1]))
+    assert g["status"][0] == 0 and list(g["bounds"][0]) == [0, 1]
+    # n = m: singletons
+    g = run_gpu(_single(np.array([5, 4, 3], f), [1, 1, 1]))
+    assert list(g["bounds"][0]) == [0, 1, 2, 3]
+    # n < m: infeasible
+    g = run_gpu(_single(np.array([5, 4], f), [1, 1, 1]))
+    assert g["status"][0] == 3 and np.all(g["bounds"][0] == -1) and np.isinf(g["obj"][0])
+    # unsorted lengths
+    g = run_gpu(_single(np.array([1, 5, 3], f), [1, 1]))
+    assert g["status"][0] == 2
+    # NaN / zero length
+    g = run_gpu(_single(np.array([5, np.nan, 3], f), [1, 1]))
+    assert g["status"][0] == 4
+    g = run_gpu(_single(np.array([5, 3, 0], f), [1, 1]))
+    assert g["status"][0] == 4
+    # unknown degree / unsorted degrees
+    g = run_gpu(_single(np.array([5, 4, 3], f), [3, 1]))
+    assert g["status"][0] == 5
+    g = run_gpu(_single(np.array([5, 4, 3], f), [1, 2]))
+    assert g["status"][0] == 2
+    # caps that cannot cover n
+    g = run_gpu(_single(np.array([5, 4, 3, 2, 1], f), [1, 1], caps=[2, 2]))
+    assert g["status"][0] == 3
+    # U32 range guard: a length above the guard is reported, never wrapped
+    g = run_gpu(_single(np.array([70000, 3], np.uint32), [1, 1], dtype="u32"))
+    assert g["status"][0] == 4
+
+
+def test_ragged_sizes_and_mixed_batch():
+    """n not a multiple of 4 or of the 128-column warp block; one bad problem in a batch
+    does not disturb the others."""
+    for n, m in [(129, 3), (130, 7), (257, 2), (383, 31), (1021, 5)]:
+        rng = np.random.default_rng(n)
+        L = wl.presort_rows(wl.predicted(rng, wl.coding_lengths(rng, (n + 7) // 8, 8)[:n])[None, :])
+        L = np.repeat(L, 3, axis=0)
+        L[1, 3], L[1, 4] = L[1, 4], L[1, 3] + 1000   # problem 1 unsorted
+        deg = wl.sorted_degree_vectors(rng, 3, m)
+        batch = wl.Batch("ragged", n, m, L.astype(np.float32), deg, wl.float_profile())
+        gpu = run_gpu(batch, keep_parents=True)
+        assert gpu["status"][1] == 2
+        for b in (0, 2):
+            ref = oracle.solve(oracle.Problem.from_batch(batch, b, mode="f32"), want_tables=True)
+            assert_exact(gpu, b, ref, batch, "f32", "minmax", check_parents=True, tag=f"ragged{n}")
+
+
+def test_host_e2e_matches_device():
+    batch = wl.config_batched(B=32, seed_problem=9)
+    gpu = run_gpu(batch)
+    pl = gpu["placer"]
+    Lh = torch.from_numpy(batch.lengths).pin_memory()
+    Dh = torch.from_numpy(batch.degrees.astype(np.int32)).pin_memory()
+    obj, bnd, st, h2d, d2h = pl.solve_host(Lh, Dh)
+    assert np.array_equal(obj.numpy().astype(np.float64), gpu["obj"])
+    assert np.array_equal(bnd.numpy(), gpu["bounds"])
+    assert h2d == batch.lengths.nbytes + batch.degrees.astype(np.int32).nbytes
+    assert d2h == 4 * batch.B + 4 * batch.B * (batch.m + 1) + 4 * batch.B
+
+
+def test_error_paths():
+    from paper_2603_28101_b200 import E_INVALID, E_STATE, HeddleError
+    from paper_2603_28101_b200.placer import Placer
+    prof = wl.float_profile()
+    pl = Placer.from_profile(prof, max_n=64, max_m=8, max_batch=4)
+    with pytest.raises(HeddleError) as e:
+        pl.backtrack()
+    assert e.value.status == E_STATE
+    L = to_dev(np.linspace(100, 1, 128, dtype=np.float32)[None, :])
+    D = to_dev(np.ones((1, 4), np.int32))
+    with pytest.raises(HeddleError) as e:   # n > max_n
+        pl.solve(L, D)
+    assert e.value.status == E_INVALID
+    pl.solve(L[:, :64], D)
+    with pytest.raises(HeddleError) as e:   # parents without HEDDLE_KEEP_PARENTS
+        pl.backtrack(parents=True)
+    assert e.value.status == E_STATE
