@@ -39,6 +39,23 @@ __global__ void __launch_bounds__(256) kern(float* out, float seed, long long* c
         unsigned x = __float_as_uint(a[q]);
         asm volatile("max.u32 %0, %0, %1;" : "+r"(x) : "r"(__float_as_uint(b[q])));
         a[q] = __uint_as_float(x);
+      } else if (OP == 6) { // FMNMX + FMUL, independent, 1:1
+        asm volatile("max.f32 %0, %0, %1;" : "+f"(a[q]) : "f"(b[q]));
+        asm volatile("mul.rn.f32 %0, %0, %1;" : "+f"(b[(q + 4) % ILP]) : "f"(b[q]));
+      } else if (OP == 7) { // FMNMX3 + FMUL 1:1
+        asm volatile("min.f32 %0, %0, %1, %2;" : "+f"(a[q]) : "f"(b[q]), "f"(b[(q + 1) % ILP]));
+        asm volatile("mul.rn.f32 %0, %0, %1;" : "+f"(b[(q + 4) % ILP]) : "f"(b[(q + 2) % ILP]));
+      } else if (OP == 8) { // cell with 2-input min: FMUL + FMNMX(max) + FMNMX(min)
+        float c0, v0;
+        asm volatile("mul.rn.f32 %0, %1, %2;" : "=f"(c0) : "f"(b[q]), "f"(a[(q + 1) % ILP]));
+        asm volatile("max.f32 %0, %1, %2;" : "=f"(v0) : "f"(c0), "f"(b[(q + 4) % ILP]));
+        asm volatile("min.f32 %0, %0, %1;" : "+f"(a[q]) : "f"(v0));
+      } else if (OP == 9) { // argmin step: FSETP + FSEL + SEL
+        float v = b[q];
+        unsigned idx = (unsigned)q;
+        asm volatile("{ .reg .pred p; setp.lt.f32 p, %2, %0; selp.f32 %0, %2, %0, p; selp.u32 %1, %3, %1, p; }"
+                     : "+f"(a[q]), "+r"(idx) : "f"(v), "r"((unsigned)it));
+        b[q] = __uint_as_float(idx) * 0.f + b[q];
       } else if (OP == 5) { // transition pair: 2x FMUL, 2x FMNMX, 1x FMNMX3
         float c0, c1, v0, v1;
         asm volatile("mul.rn.f32 %0, %1, %2;" : "=f"(c0) : "f"(b[q]), "f"(a[(q + 1) % ILP]));
@@ -98,5 +115,9 @@ int main() {
   run<4>("VIMNMX.U32", 1, nsm);
   // transition pattern: 5 instructions for 2 transitions; report instr/sm/clk
   run<5>("PAIR(2xFMUL+2xFMNMX+FMNMX3)", 5, nsm);
+  run<6>("FMNMX+FMUL", 2, nsm);
+  run<7>("FMNMX3+FMUL", 2, nsm);
+  run<8>("CELL(FMUL+FMNMX+FMNMX)", 3, nsm);
+  run<9>("ARGMIN(FSETP+FSEL+SEL)", 3, nsm);
   return 0;
 }

@@ -2,6 +2,7 @@
 from __future__ import annotations
 
 import glob
+import hashlib
 import os
 import subprocess
 import sys
@@ -27,11 +28,23 @@ def deps():
                                                                          __file__]
 
 
+STAMP = LIB + ".stamp"
+
+
+def digest() -> str:
+    h = hashlib.sha256()
+    for f in deps():
+        h.update(os.path.relpath(f, ROOT).encode())
+        h.update(open(f, "rb").read())
+    h.update(" ".join(ARCH + FLAGS).encode())
+    return h.hexdigest()
+
+
 def stale() -> bool:
-    if not os.path.exists(LIB):
+    """Content-hash check (file mtimes change when the tree is copied to a GPU box)."""
+    if not os.path.exists(LIB) or not os.path.exists(STAMP):
         return True
-    t = os.path.getmtime(LIB)
-    return any(os.path.getmtime(f) > t for f in deps())
+    return open(STAMP).read().strip() != digest()
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -41,6 +54,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
+    with open(STAMP, "w") as f:
+        f.write(digest())
     return LIB
 
 

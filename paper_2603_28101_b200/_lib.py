@@ -10,7 +10,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libheddle_place.so")
+LIB_PATH = os.environ.get("HEDDLE_PLACE_LIB") or os.path.join(_HERE, "libheddle_place.so")
 
 OK, E_INVALID, E_UNSORTED, E_INFEASIBLE, E_RANGE, E_UNKNOWN_DEGREE, E_STATE, E_CUDA, E_NCCL, E_NOMEM = range(10)
 U32, F32, F64 = 0, 1, 2

@@ -30,11 +30,17 @@
 
 namespace hp {
 
-constexpr int kLaneCols = 4;                 // columns per lane
-constexpr int kWarpCols = 32 * kLaneCols;    // columns per warp task
+constexpr int kLaneCols = 8;                 // columns per lane (R)
+constexpr int kColLanes = 8;                 // lanes across columns
+constexpr int kSplitLanes = 4;               // lanes across splits k, each owning a contiguous quarter
+constexpr int kWarpCols = kColLanes * kLaneCols;   // 64 columns per warp task
 constexpr int kGPad = 131;                   // G padding below s = 0; == 3 (mod 4) for LDS.128 alignment
-constexpr int kGTail = kWarpCols + 4;        // G padding above s = n
-constexpr int kK2Warps = 4;
+constexpr int kGTail = kWarpCols + 8;        // G padding above s = n
+constexpr int kLPad = 4 * kSplitLanes + 24;  // L / dp row padding above n (quarter rounding)
+#ifndef HEDDLE_K2_WARPS
+#define HEDDLE_K2_WARPS 4
+#endif
+constexpr int kK2Warps = HEDDLE_K2_WARPS;
 constexpr int kK2Threads = 32 * kK2Warps;
 
 struct SolveArgs {
@@ -66,15 +72,16 @@ __host__ __device__ inline int align4(int x) { return (x + 3) & ~3; }
 template <int DT, int SR>
 struct K2Smem {
   using T = Tr<DT, SR>;
-  int gOff, lOff, d0Off, d1Off, kloOff, spOff, rowOff, capOff, kvOff, total;
+  int gOff, g2Off, lOff, d0Off, d1Off, kloOff, spOff, rowOff, capOff, kvOff, total;
   __host__ __device__ K2Smem(int n, int m, bool kv) {
     int o = 0;
     auto take = [&](int bytes) { int at = o; o += (bytes + 15) & ~15; return at; };
     gOff = take((int)sizeof(typename T::G) * align4(kGPad + n + kGTail + 1));
-    lOff = take((int)sizeof(typename T::L) * align4(n + 8));
-    d0Off = take((int)sizeof(typename T::D) * align4(n + 8));
-    d1Off = take((int)sizeof(typename T::D) * align4(n + 8));
-    kloOff = kv ? take(4 * align4(n + 8)) : -1;
+    g2Off = take((int)sizeof(typename T::G) * align4(kGPad + n + kGTail + 1));   // sG2[t] = sG[t + 1]
+    lOff = take((int)sizeof(typename T::L) * align4(n + kLPad));
+    d0Off = take((int)sizeof(typename T::D) * align4(n + kLPad));
+    d1Off = take((int)sizeof(typename T::D) * align4(n + kLPad));
+    kloOff = kv ? take(4 * align4(n + kLPad)) : -1;
     spOff = kv ? take(8 * (n + 1)) : -1;
     rowOff = take(4 * m);
     capOff = take(4 * m);
@@ -90,57 +97,116 @@ __device__ __forceinline__ D shfl_down(D v, int off) { return __shfl_down_sync(0
 template <int DT> struct SpT { using type = double; };
 template <> struct SpT<HEDDLE_U32> { using type = uint64_t; };
 
-// One 4-split step of the warp sweep: columns c..c+3 of this lane, splits k..k+3.
-// Window W[x] = G[c - k - 3 + x]: W[0..3] = lo, W[4..7] = hi.
-template <int DT, int SR, bool KP, bool MASKED>
-__device__ __forceinline__ void step4(const typename Tr<DT, SR>::L* __restrict__ sL,
-                                      const typename Tr<DT, SR>::D* __restrict__ sdp, int k,
-                                      const typename Tr<DT, SR>::G (&lo)[4],
-                                      const typename Tr<DT, SR>::G (&hi)[4],
-                                      typename Tr<DT, SR>::D (&acc)[kLaneCols], int (&arg)[kLaneCols],
-                                      const int (&klo)[kLaneCols]) {
-  using T = Tr<DT, SR>;
-  typename T::D dpv[4];
-  typename T::L lv[4];
-  ld4(sdp + k, dpv);
-  ld4(sL + k, lv);
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-#pragma unroll
-    for (int r = 0; r < kLaneCols; ++r) {
-      const int x = r - u + 3;
-      const typename T::G g = x < 4 ? lo[x] : hi[x - 4];
-      typename T::D v = T::comb(dpv[u], lv[u], g);
-      if (MASKED) v = (k + u >= klo[r]) ? v : T::inf();
-      if (KP) {
-        if (v < acc[r]) { acc[r] = v; arg[r] = k + u; }   // strict '<', ascending k: lowest index
-      } else {
-        acc[r] = T::vmin(acc[r], v);
-      }
-    }
-  }
+// ---- F32 min-max fast step (the paper's Eq. 3 in the default FP32 mode) -----------------
+// Two columns share one FMUL2 (mul.rn.f32x2: L[k+u] broadcast x {G[s], G[s+1]}), so a
+// cell costs 1/2 FMA-pipe issue + FMNMX(max) + 1/2 FMNMX3(min): the ALU pipe (2 cycles
+// per FMNMX / FMNMX3) is the only bound.  The pair {G[x], G[x+1]} must sit in an aligned
+// register pair: even x comes from the natural window, odd x from a copy of G shifted by
+// one element (sG2[t] = sG[t+1]), both sliding by 4 splits per step.
+__device__ __forceinline__ unsigned long long f32x2_mul_bcast(float l, unsigned long long g2) {
+  unsigned long long l2, r;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(l2) : "f"(l));
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(l2), "l"(g2));
+  return r;
+}
+__device__ __forceinline__ float min3f(float a, float b, float c) {
+  float d;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+__device__ __forceinline__ void ld2x2(const float* p, unsigned long long (&o)[2]) {
+  const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(p);
+  o[0] = v.x;
+  o[1] = v.y;
 }
 
-// Sweep splits [k0, k1) (multiples of 4) for this lane's columns; gcol = sG + kGPad + c.
-template <int DT, int SR, bool KP, bool MASKED>
-__device__ __forceinline__ void sweep(const typename Tr<DT, SR>::L* __restrict__ sL,
-                                      const typename Tr<DT, SR>::D* __restrict__ sdp,
-                                      const typename Tr<DT, SR>::G* __restrict__ gcol, int k0, int k1,
-                                      typename Tr<DT, SR>::D (&acc)[kLaneCols], int (&arg)[kLaneCols],
-                                      const int (&klo)[kLaneCols]) {
-  if (k0 >= k1) return;
-  typename Tr<DT, SR>::G a[4], b[4];
-  ld4(gcol - k0 - 3, a);
-  ld4(gcol - k0 + 1, b);
-  int k = k0;
-#pragma unroll 1
-  for (; k + 8 <= k1; k += 8) {
-    step4<DT, SR, KP, MASKED>(sL, sdp, k, a, b, acc, arg, klo);       // window [a, b]
-    ld4(gcol - k - 7, b);                                              // low part for k + 4
-    step4<DT, SR, KP, MASKED>(sL, sdp, k + 4, b, a, acc, arg, klo);   // window [b, a]
-    ld4(gcol - k - 11, a);                                             // low part for k + 8
+// Sliding-window sweep for R columns per lane over `iters` 4-split steps starting
+// at split k (a multiple of 4).  Window W[x] = G[c - k - 3 + x], x = 0..R+3; after a
+// step it slides down by 4, so each step loads one LDS.128 of G (two in the F32
+// min-max path: G and its shifted copy) plus the LDS.128 broadcasts of dp[k..k+3]
+// and L[k..k+3].  With the loop unrolled by a multiple of the rotation period
+// (R+4)/4 the window shifts compile to register renames.
+template <int DT, int SR, bool KP, bool MASKED, int R>
+__device__ __forceinline__ void sweep_slide(const typename Tr<DT, SR>::L* __restrict__ sL,
+                                            const typename Tr<DT, SR>::D* __restrict__ sdp,
+                                            const typename Tr<DT, SR>::G* __restrict__ gcol,
+                                            const typename Tr<DT, SR>::G* __restrict__ gcol2, int k, int iters,
+                                            typename Tr<DT, SR>::D (&acc)[R], int (&arg)[R], const int (&klo)[R]) {
+  using T = Tr<DT, SR>;
+  if constexpr (DT == HEDDLE_F32 && SR == HEDDLE_MINMAX && !KP && !MASKED) {
+    static_assert(R % 2 == 0, "column pairs");
+    constexpr int P = (R + 4) / 2;          // register pairs per window
+    unsigned long long wp[P], vp[P];        // wp[q] = {W[2q], W[2q+1]}, vp[q] = {W[2q+1], W[2q+2]}
+    const float* gk = gcol - k - 3;
+    const float* gk2 = gcol2 - k - 3;
+#pragma unroll
+    for (int q = 0; q < P; q += 2) {
+      ld2x2(gk + 2 * q, *reinterpret_cast<unsigned long long(*)[2]>(&wp[q]));
+      ld2x2(gk2 + 2 * q, *reinterpret_cast<unsigned long long(*)[2]>(&vp[q]));
+    }
+#pragma unroll 4
+    for (int t = 0; t < iters; ++t) {
+      float dpv[4], lv[4];
+      ld4(sdp + k, dpv);
+      ld4(sL + k, lv);
+      float v[4][R];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+#pragma unroll
+        for (int r = 0; r < R; r += 2) {
+          const int x = r - u + 3;           // cells (u, r), (u, r+1) use W[x], W[x+1]
+          const unsigned long long g2 = (x % 2 == 0) ? wp[x / 2] : vp[(x - 1) / 2];
+          const unsigned long long c2 = f32x2_mul_bcast(lv[u], g2);
+          float c0, c1;
+          asm("mov.b64 {%0, %1}, %2;" : "=f"(c0), "=f"(c1) : "l"(c2));
+          v[u][r] = fmaxf(dpv[u], c0);
+          v[u][r + 1] = fmaxf(dpv[u], c1);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        acc[r] = min3f(acc[r], v[0][r], v[1][r]);
+        acc[r] = min3f(acc[r], v[2][r], v[3][r]);
+      }
+#pragma unroll
+      for (int q = P - 1; q >= 2; --q) { wp[q] = wp[q - 2]; vp[q] = vp[q - 2]; }
+      k += 4;
+      gk -= 4;
+      gk2 -= 4;
+      ld2x2(gk, *reinterpret_cast<unsigned long long(*)[2]>(&wp[0]));
+      ld2x2(gk2, *reinterpret_cast<unsigned long long(*)[2]>(&vp[0]));
+    }
+  } else {
+    typename T::G w[R + 4];
+    const typename T::G* gk = gcol - k - 3;
+#pragma unroll
+    for (int x = 0; x < R + 4; x += 4) ld4(gk + x, *reinterpret_cast<typename T::G(*)[4]>(&w[x]));
+#pragma unroll 4
+    for (int t = 0; t < iters; ++t) {
+      typename T::D dpv[4];
+      typename T::L lv[4];
+      ld4(sdp + k, dpv);
+      ld4(sL + k, lv);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          typename T::D v = T::comb(dpv[u], lv[u], w[r - u + 3]);
+          if (MASKED) v = (k + u >= klo[r]) ? v : T::inf();
+          if (KP) {
+            if (v < acc[r]) { acc[r] = v; arg[r] = k + u; }   // strict '<', ascending k: lowest index
+          } else {
+            acc[r] = T::vmin(acc[r], v);
+          }
+        }
+      }
+#pragma unroll
+      for (int x = R + 3; x >= 4; --x) w[x] = w[x - 4];
+      k += 4;
+      gk -= 4;
+      ld4(gk, *reinterpret_cast<typename T::G(*)[4]>(&w[0]));
+    }
   }
-  if (k < k1) step4<DT, SR, KP, MASKED>(sL, sdp, k, a, b, acc, arg, klo);
 }
 
 template <int DT, int SR, bool KP, bool KV>
@@ -155,6 +221,7 @@ __global__ void __launch_bounds__(kK2Threads) k2_dp_batched(SolveArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const K2Smem<DT, SR> lay(n, m, KV);
   G* sG = reinterpret_cast<G*>(smem + lay.gOff);
+  G* sG2 = reinterpret_cast<G*>(smem + lay.g2Off);
   L* sL = reinterpret_cast<L*>(smem + lay.lOff);
   D* const sdp0 = reinterpret_cast<D*>(smem + lay.d0Off);
   D* const sdp1 = reinterpret_cast<D*>(smem + lay.d1Off);
@@ -175,16 +242,17 @@ __global__ void __launch_bounds__(kK2Threads) k2_dp_batched(SolveArgs a) {
   // ---------------- load + validate (lengths sorted/finite/positive, degrees known and sorted)
   if (tid == 0) s_err = INT_MAX;
   __syncthreads();
+  for (int t = tid; t < n; t += kK2Threads) sL[t] = gL[t];                       // coalesced, batched
+  for (int t = n + tid; t < align4(n + kLPad); t += kK2Threads) sL[t] = (L)1;  // finite pad: no 0*inf
+  __syncthreads();
   for (int t = tid; t < n; t += kK2Threads) {
-    L x = gL[t];
-    sL[t] = x;
+    const L x = sL[t];
     bool bad_range;
     if constexpr (DT == HEDDLE_U32) bad_range = (x == 0u) || (x > a.lmax_u32);
     else bad_range = !(x > (L)0) || !(x < (L)INFINITY);
     if (bad_range) atomicMin(&s_err, (int)HEDDLE_E_RANGE);
-    else if (t + 1 < n && gL[t + 1] > x) atomicMin(&s_err, (int)HEDDLE_E_UNSORTED);
+    else if (t + 1 < n && sL[t + 1] > x) atomicMin(&s_err, (int)HEDDLE_E_UNSORTED);
   }
-  for (int t = n + tid; t < align4(n + 8); t += kK2Threads) sL[t] = (L)1;  // finite pad: no 0*inf
   for (int j = tid; j < m; j += kK2Threads) {
     const int d = a.degrees[(int64_t)b * a.ds + j];
     int row = -1;
@@ -219,7 +287,7 @@ __global__ void __launch_bounds__(kK2Threads) k2_dp_batched(SolveArgs a) {
     S* gSp = reinterpret_cast<S*>(a.spws) + (int64_t)b * (n + 1);   // for the backtrack
     for (int t = tid; t <= n; t += kK2Threads) gSp[t] = sSp[t];
   }
-  for (int t = tid; t < align4(n + 8); t += kK2Threads) { sdp0[t] = T::inf(); sdp1[t] = T::inf(); }
+  for (int t = tid; t < align4(n + kLPad); t += kK2Threads) { sdp0[t] = T::inf(); sdp1[t] = T::inf(); }
 
   // ---------------- layers
   for (int j = 1; j <= m; ++j) {
@@ -227,14 +295,19 @@ __global__ void __launch_bounds__(kK2Threads) k2_dp_batched(SolveArgs a) {
     D* const cur = (j & 1) ? sdp1 : sdp0;
     const int imax_layer = n - m + j;                  // computed region [j, n-m+j]
     // cost table of worker j: G_j[s] for s = 1..min(n, cap), +inf padding elsewhere
-    {
+    // (rebuilt only when the worker's profile row or cap changes: sorted degree
+    //  vectors over a few MP degrees change row at most D-1 times per problem)
+    if (j == 1 || srow[j - 1] != srow[j - 2] || scap[j - 1] != scap[j - 2]) {
       const G* grow = gtab + (int64_t)srow[j - 1] * a.gstride;
       const int cap = scap[j - 1];
       const int hi = (cap >= 0 && cap < n) ? cap : n;
       for (int t = tid; t < kGPad + n + kGTail + 1; t += kK2Threads) {
         const int s = t - kGPad;
-        sG[t] = (s >= 1 && s <= hi) ? grow[s] : T::gpad();
+        const G g = (s >= 1 && s <= hi) ? grow[s] : T::gpad();
+        sG[t] = g;
+        if (t > 0) sG2[t - 1] = g;
       }
+      if (tid == 0) sG2[kGPad + n + kGTail] = T::gpad();
     }
     if constexpr (KV) {
       const int64_t kvc = skv[j - 1];
@@ -302,40 +375,52 @@ __global__ void __launch_bounds__(kK2Threads) k2_dp_batched(SolveArgs a) {
       const int cbase = j & ~3;
       const int nblk = (imax_layer - cbase) / kWarpCols + 1;
       const int kstart = (j - 1) & ~3;
+      const int cl = lane & (kColLanes - 1), kg = lane / kColLanes;
       for (;;) {
         int t = 0;
         if (lane == 0) t = atomicAdd(&s_ctr, 1);
         t = __shfl_sync(0xffffffffu, t, 0);
         if (t >= nblk) break;
-        const int cb = cbase + kWarpCols * (nblk - 1 - t);   // longest block first
-        const int c = cb + kLaneCols * lane;
+        const int cb = cbase + kWarpCols * (nblk - 1 - t);   // longest block first (LPT)
+        const int c = cb + kLaneCols * cl;
         const int imax = min(cb + kWarpCols - 1, imax_layer);
-        const int kend = align4(imax);
+        const int kend = align4(imax);                       // splits k <= imax - 1
+        // split-lane group kg sweeps the contiguous quarter [kstart + kg*Q, kstart + (kg+1)*Q)
+        const int Q = 4 * ((kend - kstart + 4 * kSplitLanes - 1) / (4 * kSplitLanes));
         D acc[kLaneCols];
         int arg[kLaneCols], klo[kLaneCols];
 #pragma unroll
         for (int r = 0; r < kLaneCols; ++r) { acc[r] = T::inf(); arg[r] = -1; klo[r] = j - 1; }
-        const G* gcol = sG + kGPad + c;
         if constexpr (KV) {
 #pragma unroll
           for (int r = 0; r < kLaneCols; ++r) klo[r] = sklo[min(max(c + r, j), imax)];
-          const int kA = __reduce_min_sync(0xffffffffu, klo[0]);
-          const int kB = __reduce_max_sync(0xffffffffu, klo[kLaneCols - 1]);
-          const int ka = max(kstart, kA & ~3);
-          const int kb = max(ka, min(kend, align4(kB)));
-          sweep<DT, SR, KP, true>(sL, prev, gcol, ka, kb, acc, arg, klo);
-          sweep<DT, SR, KP, false>(sL, prev, gcol, kb, kend, acc, arg, klo);
-        } else {
-          sweep<DT, SR, KP, false>(sL, prev, gcol, kstart, kend, acc, arg, klo);
         }
+        sweep_slide<DT, SR, KP, KV, kLaneCols>(sL, prev, sG + kGPad + c, sG2 + kGPad + c, kstart + kg * Q, Q / 4,
+                                               acc, arg, klo);
+        // combine the kSplitLanes partial minima of each column (lowest split on ties)
 #pragma unroll
-        for (int r = 0; r < kLaneCols; ++r) {
-          const int i = c + r;
-          if (i >= j && i <= imax_layer) {
-            const D v = T::norm(acc[r]);
-            cur[i] = v;
-            gdp[(int64_t)j * (n + 1) + i] = v;
-            if (KP) gpar[(int64_t)j * (n + 1) + i] = (v == T::inf()) ? -1 : arg[r];
+        for (int off = kColLanes; off < 32; off <<= 1) {
+#pragma unroll
+          for (int r = 0; r < kLaneCols; ++r) {
+            const D ov = __shfl_xor_sync(0xffffffffu, acc[r], off);
+            if (KP) {
+              const int oa = __shfl_xor_sync(0xffffffffu, arg[r], off);
+              if (ov < acc[r] || (ov == acc[r] && (unsigned)oa < (unsigned)arg[r])) { acc[r] = ov; arg[r] = oa; }
+            } else {
+              acc[r] = T::vmin(acc[r], ov);
+            }
+          }
+        }
+        if (kg == 0) {
+#pragma unroll
+          for (int r = 0; r < kLaneCols; ++r) {
+            const int i = c + r;
+            if (i >= j && i <= imax_layer) {
+              const D v = T::norm(acc[r]);
+              cur[i] = v;
+              gdp[(int64_t)j * (n + 1) + i] = v;
+              if (KP) gpar[(int64_t)j * (n + 1) + i] = (v == T::inf()) ? -1 : arg[r];
+            }
           }
         }
       }

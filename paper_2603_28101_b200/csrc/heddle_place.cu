@@ -58,6 +58,7 @@ struct heddle_place_ctx {
   SolveArgs last{};
   int64_t launches = 0;
   int smem_optin = 0;
+  int k2_smem_max = 0;
 };
 
 namespace {
@@ -260,11 +261,19 @@ heddle_status heddle_place_init(const heddle_place_config* c, heddle_place_ctx**
     return HEDDLE_E_CUDA;
   }
   // opt in to large dynamic shared memory for every K2 variant this ctx may launch
+  // (the dynamic limit is the opt-in maximum minus the kernel's static shared memory)
   for (int kp = 0; kp < 2; ++kp)
-    for (int kv = 0; kv < 2; ++kv)
-      cudaFuncSetAttribute(k2_for(x->dtype, x->semiring, kp, kv), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           x->smem_optin);
-  cudaGetLastError();
+    for (int kv = 0; kv < 2; ++kv) {
+      const void* fn = reinterpret_cast<const void*>(k2_for(x->dtype, x->semiring, kp, kv));
+      cudaFuncAttributes fa{};
+      if (cudaFuncGetAttributes(&fa, fn) != cudaSuccess ||
+          cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               x->smem_optin - (int)fa.sharedSizeBytes) != cudaSuccess) {
+        heddle_place_destroy(x);
+        return HEDDLE_E_CUDA;
+      }
+      x->k2_smem_max = x->smem_optin - (int)fa.sharedSizeBytes;
+    }
   *out = x;
   return HEDDLE_OK;
 }
@@ -279,7 +288,7 @@ heddle_status heddle_place_solve(heddle_place_ctx* x, const heddle_place_problem
   const bool kv = p->kv_caps != nullptr;
   const bool kp = (x->flags & HEDDLE_KEEP_PARENTS) != 0;
   const int smem = k2_smem(x->dtype, x->semiring, p->n, p->m, kv);
-  if (smem > x->smem_optin) return HEDDLE_E_INVALID;   // n too large for the one-CTA-per-problem kernel
+  if (smem > x->k2_smem_max) return HEDDLE_E_INVALID;   // n too large for the one-CTA-per-problem kernel
   DeviceGuard guard(x->device);
   SolveArgs a{};
   a.n = p->n;
