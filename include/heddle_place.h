@@ -77,7 +77,12 @@ typedef enum { HEDDLE_U32 = 0, HEDDLE_F32 = 1, HEDDLE_F64 = 2 } heddle_dtype;
 typedef enum { HEDDLE_MINMAX = 0 /* Eq. 3, default */, HEDDLE_MINPLUS = 1 } heddle_semiring;
 
 /* config.flags */
-#define HEDDLE_KEEP_PARENTS 0x1u  /* solve records every back-pointer (slower inner loop) */
+#define HEDDLE_KEEP_PARENTS 0x1u  /* solve records every back-pointer (slower inner loop).  With
+                                     the layered kernel this needs 32-bit dp values (F32, U32
+                                     MINMAX); F64 / U32-MINPLUS parents need the batched kernel. */
+#define HEDDLE_FORCE_BATCHED 0x2u /* always use the one-CTA-per-problem kernel (E_INVALID if n is
+                                     too large for shared memory); default: chosen per call    */
+#define HEDDLE_FORCE_LAYERED 0x4u /* always use the layered multi-CTA-per-problem kernel       */
 
 typedef struct heddle_place_ctx heddle_place_ctx;
 

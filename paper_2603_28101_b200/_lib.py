@@ -16,6 +16,9 @@ OK, E_INVALID, E_UNSORTED, E_INFEASIBLE, E_RANGE, E_UNKNOWN_DEGREE, E_STATE, E_C
 U32, F32, F64 = 0, 1, 2
 MINMAX, MINPLUS = 0, 1
 KEEP_PARENTS = 0x1
+FORCE_BATCHED = 0x2
+FORCE_LAYERED = 0x4
+KERNELS = {"auto": 0, "batched": FORCE_BATCHED, "layered": FORCE_LAYERED}
 
 DTYPES = {"u32": U32, "f32": F32, "f64": F64}
 SEMIRINGS = {"minmax": MINMAX, "minplus": MINPLUS}

@@ -1,0 +1,331 @@
+// K3 -- layered presorted DP for large n or few problems: one launch per DP layer,
+// the layer's (column, split) triangle cut into uniform tiles spread over every SM.
+//
+// Same recurrence and arithmetic as K2 (Eq. 3; traits.cuh).  A tile is
+// (problem b, 256 consecutive columns, a chunk of KC splits); the CTA stages
+// dp[j-1][k0..k1), L[k0..k1) and the G window it needs (plus the one-element
+// shifted copy for the FMUL2 column pairs) in shared memory, its 4 warps run the K2
+// sliding sweep (64 columns each, 4 split quarters), and the per-column partial
+// minima of the chunk are merged into dp[j][i] with atomicMin on the value's bit
+// pattern (all values are non-negative, so the unsigned order is the value order;
+// KEEP_PARENTS merges (value << 32 | k) so ties keep the lowest split).
+// Persistent grid (SMs x occupancy), grid-stride over tiles.  The split mode of
+// the multi-GPU driver restricts the columns a rank computes ([col_lo, col_hi)
+// blocks) and exchanges finished rows between layers.
+#pragma once
+#include "dp_batched.cuh"
+
+namespace hp {
+
+constexpr int kK3Warps = 4;
+constexpr int kK3Threads = 32 * kK3Warps;
+constexpr int kK3Cols = kK3Warps * kWarpCols;   // 256 columns per tile
+constexpr int kK3GPadLo = 23;                    // == 3 (mod 4): G staging below c0 - k1
+constexpr int kK3LPad = 24;
+
+struct LayerArgs {
+  SolveArgs a;
+  int j;            // layer being computed (2..m)
+  int kc;           // splits per tile (multiple of 16)
+  int ncb;          // column blocks per problem
+  int nq;           // split chunks per column block (max)
+  int blk_lo, blk_hi;   // column blocks [blk_lo, blk_hi) owned by this launch (split mode), else [0, ncb)
+  int blk_stride;   // block ownership: block b owned iff (b in [blk_lo, blk_hi)) -- contiguous
+  const int32_t* klo;   // [B][n+1] kv lower bounds for this layer, or null
+  unsigned long long* keys;   // [B][n+1] packed (value, split) minima (KEEP_PARENTS), or null
+};
+
+template <class D> struct AtomicBits;
+template <> struct AtomicBits<float> {
+  __device__ static void amin(float* p, float v) { atomicMin(reinterpret_cast<unsigned*>(p), __float_as_uint(v)); }
+  __device__ static uint32_t bits(float v) { return __float_as_uint(v); }
+  __device__ static float from(uint32_t b) { return __uint_as_float(b); }
+};
+template <> struct AtomicBits<uint32_t> {
+  __device__ static void amin(uint32_t* p, uint32_t v) { atomicMin(p, v); }
+  __device__ static uint32_t bits(uint32_t v) { return v; }
+  __device__ static uint32_t from(uint32_t b) { return b; }
+};
+template <> struct AtomicBits<double> {
+  __device__ static void amin(double* p, double v) {
+    atomicMin(reinterpret_cast<unsigned long long*>(p), (unsigned long long)__double_as_longlong(v));
+  }
+};
+template <> struct AtomicBits<uint64_t> {
+  __device__ static void amin(uint64_t* p, uint64_t v) {
+    atomicMin(reinterpret_cast<unsigned long long*>(p), (unsigned long long)v);
+  }
+};
+
+// ---------------------------------------------------------------- fill (+inf rows, -1 parents)
+template <int DT, int SR>
+__global__ void k3_fill(SolveArgs a, int64_t cells) {
+  using T = Tr<DT, SR>;
+  using D = typename T::D;
+  D* dp = reinterpret_cast<D*>(a.dpws);
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < cells; t += (int64_t)gridDim.x * blockDim.x) {
+    dp[t] = T::inf();
+    if (a.parws) a.parws[t] = -1;
+  }
+}
+
+// ---------------------------------------------------------------- prologue: validate, Sp, layer 1
+template <int DT, int SR, bool KP, bool KV>
+__global__ void __launch_bounds__(256) k3_prologue(SolveArgs a) {
+  using T = Tr<DT, SR>;
+  using L = typename T::L;
+  using G = typename T::G;
+  using D = typename T::D;
+  using S = typename SpT<DT>::type;
+  const int n = a.n, m = a.m, b = blockIdx.x, tid = threadIdx.x;
+  __shared__ int s_err;
+  const L* gL = reinterpret_cast<const L*>(a.lengths) + (int64_t)b * a.ls;
+  if (tid == 0) s_err = INT_MAX;
+  __syncthreads();
+  for (int t = tid; t < n; t += blockDim.x) {
+    const L x = gL[t];
+    bool bad_range;
+    if constexpr (DT == HEDDLE_U32) bad_range = (x == 0u) || (x > a.lmax_u32);
+    else bad_range = !(x > (L)0) || !(x < (L)INFINITY);
+    if (bad_range) atomicMin(&s_err, (int)HEDDLE_E_RANGE);
+    else if (t + 1 < n && gL[t + 1] > x) atomicMin(&s_err, (int)HEDDLE_E_UNSORTED);
+  }
+  int row1 = 0;
+  for (int j = tid; j < m; j += blockDim.x) {
+    const int d = a.degrees[(int64_t)b * a.ds + j];
+    int row = -1;
+    for (int q = 0; q < a.D; ++q) row = (a.prof_deg[q] == d) ? q : row;
+    if (row < 0) atomicMin(&s_err, (int)HEDDLE_E_UNKNOWN_DEGREE);
+    if (j + 1 < m && a.degrees[(int64_t)b * a.ds + j + 1] > d) atomicMin(&s_err, (int)HEDDLE_E_UNSORTED);
+  }
+  __syncthreads();
+  int err = s_err == INT_MAX ? 0 : s_err;
+  if (err == 0 && n < m) err = HEDDLE_E_INFEASIBLE;
+  if (tid == 0) {
+    a.status[b] = err;   // OK for now; the finaliser turns +inf into INFEASIBLE
+    if (err != 0 && a.status_out) a.status_out[b] = err;
+  }
+  if (err != 0) return;
+  {
+    const int d = a.degrees[(int64_t)b * a.ds];
+    for (int q = 0; q < a.D; ++q) row1 = (a.prof_deg[q] == d) ? q : row1;
+  }
+  S* gSp = KV ? reinterpret_cast<S*>(a.spws) + (int64_t)b * (n + 1) : nullptr;
+  if constexpr (KV) {   // left-to-right prefix sums (R6): one thread, exact order
+    if (tid == 0) {
+      S acc = 0;
+      gSp[0] = 0;
+      for (int t = 0; t < n; ++t) { acc += (S)gL[t]; gSp[t + 1] = acc; }
+    }
+    __syncthreads();
+  }
+  // layer 1: dp[1][i] = L(tau_1) T F(i) for i in [1, n-m+1]
+  const G* grow = reinterpret_cast<const G*>(a.gtab) + (int64_t)row1 * a.gstride;
+  const int cap = a.caps ? a.caps[(int64_t)b * a.cs] : -1;
+  const int64_t kvc = KV ? a.kv[(int64_t)b * a.kvs] : -1;
+  D* gdp = reinterpret_cast<D*>(a.dpws) + (int64_t)b * (m + 1) * (n + 1);
+  const L l0 = gL[0];
+  for (int i = 1 + tid; i <= n - m + 1; i += blockDim.x) {
+    D v = T::comb(T::zero(), l0, (cap >= 0 && i > cap) ? T::gpad() : grow[i]);
+    if constexpr (KV) { if (kvc >= 0 && gSp[i] - gSp[0] > (S)kvc) v = T::inf(); }
+    v = T::norm(v);
+    gdp[(int64_t)(n + 1) + i] = v;
+    if (KP) a.parws[(int64_t)b * (m + 1) * (n + 1) + (n + 1) + i] = (v == T::inf()) ? -1 : 0;
+  }
+}
+
+// ---------------------------------------------------------------- kv lower bounds for layer j
+template <int DT>
+__global__ void k3_klo(SolveArgs a, int j, int32_t* klo) {
+  using S = typename SpT<DT>::type;
+  const int n = a.n, m = a.m;
+  const int b = blockIdx.y;
+  const S* gSp = reinterpret_cast<const S*>(a.spws) + (int64_t)b * (n + 1);
+  const int64_t kvc = a.kv[(int64_t)b * a.kvs + j - 1];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += gridDim.x * blockDim.x) {
+    int lo = j - 1;
+    if (kvc >= 0 && i >= j && i <= n - m + j) {
+      int l = j - 1, h = i;
+      while (l < h) {
+        int mid = (l + h) >> 1;
+        if (gSp[i] - gSp[mid] <= (S)kvc) h = mid; else l = mid + 1;
+      }
+      lo = l;
+    }
+    klo[(int64_t)b * (n + 1) + i] = lo;
+  }
+}
+
+// ---------------------------------------------------------------- one layer, tiled
+template <int DT, int SR>
+struct K3Smem {
+  using T = Tr<DT, SR>;
+  int lOff, dOff, gOff, g2Off, total, gLen;
+  __host__ __device__ K3Smem(int kc) {
+    int o = 0;
+    auto take = [&](int bytes) { int at = o; o += (bytes + 15) & ~15; return at; };
+    gLen = align4(kK3Cols + kc + kK3GPadLo + 16);
+    lOff = take((int)sizeof(typename T::L) * (kc + kK3LPad));
+    dOff = take((int)sizeof(typename T::D) * (kc + kK3LPad));
+    gOff = take((int)sizeof(typename T::G) * gLen);
+    g2Off = take((int)sizeof(typename T::G) * gLen);
+    total = o;
+  }
+};
+
+template <int DT, int SR, bool KP, bool KV>
+__global__ void __launch_bounds__(kK3Threads) k3_layer(LayerArgs la) {
+  using T = Tr<DT, SR>;
+  using L = typename T::L;
+  using G = typename T::G;
+  using D = typename T::D;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const SolveArgs& a = la.a;
+  const int n = a.n, m = a.m, j = la.j, kc = la.kc;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int cl = lane & (kColLanes - 1), kg = lane / kColLanes;
+  const K3Smem<DT, SR> lay(kc);
+  L* sL = reinterpret_cast<L*>(smem + lay.lOff);
+  D* sdp = reinterpret_cast<D*>(smem + lay.dOff);
+  G* sG = reinterpret_cast<G*>(smem + lay.gOff);
+  G* sG2 = reinterpret_cast<G*>(smem + lay.g2Off);
+  const int imax_layer = n - m + j;
+  const int cbase = j & ~3;
+  const int kstart = (j - 1) & ~3;
+  const int nblk = la.blk_hi - la.blk_lo;
+  const int64_t ntiles = (int64_t)a.B * nblk * la.nq;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int q = (int)(tile % la.nq);
+    const int blk = la.blk_lo + (int)((tile / la.nq) % nblk);
+    const int b = (int)(tile / ((int64_t)la.nq * nblk));
+    const int c0 = cbase + kK3Cols * blk;
+    if (c0 > imax_layer) continue;                              // (uniform across the CTA)
+    const int imaxb = min(c0 + kK3Cols - 1, imax_layer);
+    const int kend = align4(imaxb);
+    const int k0 = kstart + q * kc;
+    if (k0 >= kend) continue;
+    const int k1 = min(k0 + kc, kend);
+    if (a.status[b] != HEDDLE_OK) continue;
+    const L* gL = reinterpret_cast<const L*>(a.lengths) + (int64_t)b * a.ls;
+    const D* gprev = reinterpret_cast<const D*>(a.dpws) + ((int64_t)b * (m + 1) + (j - 1)) * (n + 1);
+    D* gcur = reinterpret_cast<D*>(a.dpws) + ((int64_t)b * (m + 1) + j) * (n + 1);
+    int row = 0;
+    const int d = a.degrees[(int64_t)b * a.ds + j - 1];
+    for (int qq = 0; qq < a.D; ++qq) row = (a.prof_deg[qq] == d) ? qq : row;
+    const G* grow = reinterpret_cast<const G*>(a.gtab) + (int64_t)row * a.gstride;
+    const int cap = a.caps ? a.caps[(int64_t)b * a.cs + j - 1] : -1;
+    const int ghi = (cap >= 0 && cap < n) ? cap : n;
+    // ---- stage: splits [k0, k1) (+inf / 1 beyond k1 so quarter overruns contribute nothing)
+    __syncthreads();   // previous tile's readers are done
+    for (int t = tid; t < kc + kK3LPad; t += kK3Threads) {
+      const int k = k0 + t;
+      const bool in = k < k1;
+      sdp[t] = in ? gprev[k] : T::inf();
+      sL[t] = in ? gL[k] : (L)1;
+    }
+    // G(s) for s in [s0, s0 + gLen], s0 = c0 - k1 - kK3GPadLo (== 1 mod 4: window alignment)
+    const int s0 = c0 - k1 - kK3GPadLo;
+    for (int t = tid; t <= lay.gLen; t += kK3Threads) {
+      const int s = s0 + t;
+      const G g = (s >= 1 && s <= ghi) ? grow[s] : T::gpad();
+      if (t < lay.gLen) sG[t] = g;
+      if (t > 0) sG2[t - 1] = g;
+    }
+    __syncthreads();
+    // ---- sweep: warp w owns columns [c0 + 64 w, c0 + 64 w + 64)
+    const int cw = c0 + kWarpCols * warp;
+    if (cw <= imaxb) {
+      const int c = cw + kLaneCols * cl;
+      const int Q = 4 * ((k1 - k0 + 4 * kSplitLanes - 1) / (4 * kSplitLanes));
+      D acc[kLaneCols];
+      int arg[kLaneCols], klo[kLaneCols];
+#pragma unroll
+      for (int r = 0; r < kLaneCols; ++r) { acc[r] = T::inf(); arg[r] = -1; klo[r] = j - 1; }
+      if constexpr (KV) {
+#pragma unroll
+        for (int r = 0; r < kLaneCols; ++r) klo[r] = la.klo[(int64_t)b * (n + 1) + min(max(c + r, j), imaxb)];
+      }
+      // shifted bases: sdpb[k] = sdp[k - k0]; gcol - k - 3 = &G(c - k - 3)
+      sweep_slide<DT, SR, KP, KV, kLaneCols>(sL - k0, sdp - k0, sG + (c - s0), sG2 + (c - s0), k0 + kg * Q, Q / 4,
+                                             acc, arg, klo);
+#pragma unroll
+      for (int off = kColLanes; off < 32; off <<= 1) {
+#pragma unroll
+        for (int r = 0; r < kLaneCols; ++r) {
+          const D ov = __shfl_xor_sync(0xffffffffu, acc[r], off);
+          if (KP) {
+            const int oa = __shfl_xor_sync(0xffffffffu, arg[r], off);
+            if (ov < acc[r] || (ov == acc[r] && (unsigned)oa < (unsigned)arg[r])) { acc[r] = ov; arg[r] = oa; }
+          } else {
+            acc[r] = T::vmin(acc[r], ov);
+          }
+        }
+      }
+      if (kg == 0) {
+#pragma unroll
+        for (int r = 0; r < kLaneCols; ++r) {
+          const int i = c + r;
+          if (i >= j && i <= imaxb) {
+            const D v = T::norm(acc[r]);
+            if constexpr (KP) {
+              // (value, split) packed: lowest value, then lowest split (32-bit value types only)
+              if constexpr (sizeof(D) == 4) {
+                if (v != T::inf()) {
+                  const unsigned long long key = ((unsigned long long)AtomicBits<D>::bits(v) << 32) | (unsigned)arg[r];
+                  atomicMin(la.keys + (int64_t)b * (n + 1) + i, key);
+                }
+              }
+            } else {
+              if (v != T::inf()) AtomicBits<D>::amin(gcur + i, v);
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- KEEP_PARENTS: unpack keys of layer j
+template <int DT, int SR>
+__global__ void k3_unpack(SolveArgs a, int j, unsigned long long* keys) {
+  using T = Tr<DT, SR>;
+  using D = typename T::D;
+  const int n = a.n, m = a.m, b = blockIdx.y;
+  if constexpr (sizeof(D) == 4) {
+    D* gcur = reinterpret_cast<D*>(a.dpws) + ((int64_t)b * (m + 1) + j) * (n + 1);
+    int32_t* pcur = a.parws + ((int64_t)b * (m + 1) + j) * (n + 1);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += gridDim.x * blockDim.x) {
+      unsigned long long& key = keys[(int64_t)b * (n + 1) + i];
+      if (key != ~0ull) {
+        gcur[i] = AtomicBits<D>::from((uint32_t)(key >> 32));
+        pcur[i] = (int32_t)(key & 0xffffffffu);
+      }
+      key = ~0ull;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- finaliser
+template <int DT, int SR>
+__global__ void k3_finalize(SolveArgs a) {
+  using T = Tr<DT, SR>;
+  using D = typename T::D;
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= a.B) return;
+  const int n = a.n, m = a.m;
+  if (a.status[b] != HEDDLE_OK) {
+    if constexpr (DT == HEDDLE_U32 && SR == HEDDLE_MINPLUS) reinterpret_cast<uint64_t*>(a.objective)[b] = ~0ull;
+    else reinterpret_cast<D*>(a.objective)[b] = T::inf();
+    return;
+  }
+  const D obj = reinterpret_cast<const D*>(a.dpws)[((int64_t)b * (m + 1) + m) * (n + 1) + n];
+  const int st = (obj == T::inf()) ? (int)HEDDLE_E_INFEASIBLE : (int)HEDDLE_OK;
+  a.status[b] = st;
+  if (a.status_out) a.status_out[b] = st;
+  if constexpr (DT == HEDDLE_U32 && SR == HEDDLE_MINPLUS)
+    reinterpret_cast<uint64_t*>(a.objective)[b] = (obj == T::inf()) ? ~0ull : obj;
+  else
+    reinterpret_cast<D*>(a.objective)[b] = obj;
+}
+
+}  // namespace hp

@@ -13,6 +13,7 @@
 
 #include "backtrack.cuh"
 #include "dp_batched.cuh"
+#include "dp_layered.cuh"
 #include "heddle_place.h"
 
 using namespace hp;
@@ -59,6 +60,10 @@ struct heddle_place_ctx {
   int64_t launches = 0;
   int smem_optin = 0;
   int k2_smem_max = 0;
+  int num_sms = 0;
+  int32_t* d_klo = nullptr;             // [max_batch][max_n+1] (layered kernel, kv caps)
+  unsigned long long* d_keys = nullptr; // [max_batch][max_n+1] (layered kernel, KEEP_PARENTS)
+  bool last_layered = false;
 };
 
 namespace {
@@ -104,10 +109,55 @@ K4Fn k4_for(int dt, int sr, bool kv) {
   return sr == HEDDLE_MINMAX ? pick_k4<HEDDLE_U32, HEDDLE_MINMAX>(kv) : pick_k4<HEDDLE_U32, HEDDLE_MINPLUS>(kv);
 }
 
+using K3Fn = void (*)(LayerArgs);
+using KPro = void (*)(SolveArgs);
+template <int DT, int SR>
+K3Fn pick_k3(bool kp, bool kv) {
+  if (kp) return kv ? k3_layer<DT, SR, true, true> : k3_layer<DT, SR, true, false>;
+  return kv ? k3_layer<DT, SR, false, true> : k3_layer<DT, SR, false, false>;
+}
+template <int DT, int SR>
+KPro pick_pro(bool kp, bool kv) {
+  if (kp) return kv ? k3_prologue<DT, SR, true, true> : k3_prologue<DT, SR, true, false>;
+  return kv ? k3_prologue<DT, SR, false, true> : k3_prologue<DT, SR, false, false>;
+}
+#define HP_DISPATCH(NAME, ...)                                                                          \
+  (dt == HEDDLE_F32 ? (sr == HEDDLE_MINMAX ? NAME<HEDDLE_F32, HEDDLE_MINMAX>(__VA_ARGS__)               \
+                                           : NAME<HEDDLE_F32, HEDDLE_MINPLUS>(__VA_ARGS__))             \
+   : dt == HEDDLE_F64 ? (sr == HEDDLE_MINMAX ? NAME<HEDDLE_F64, HEDDLE_MINMAX>(__VA_ARGS__)             \
+                                             : NAME<HEDDLE_F64, HEDDLE_MINPLUS>(__VA_ARGS__))           \
+                      : (sr == HEDDLE_MINMAX ? NAME<HEDDLE_U32, HEDDLE_MINMAX>(__VA_ARGS__)             \
+                                             : NAME<HEDDLE_U32, HEDDLE_MINPLUS>(__VA_ARGS__)))
+K3Fn k3_for(int dt, int sr, bool kp, bool kv) { return HP_DISPATCH(pick_k3, kp, kv); }
+KPro pro_for(int dt, int sr, bool kp, bool kv) { return HP_DISPATCH(pick_pro, kp, kv); }
+template <int DT, int SR> int k3_smem_t(int kc) { return K3Smem<DT, SR>(kc).total; }
+int k3_smem(int dt, int sr, int kc) { return HP_DISPATCH(k3_smem_t, kc); }
+
 int k2_smem(int dt, int sr, int n, int m, bool kv) {
   if (dt == HEDDLE_F32) return sr == HEDDLE_MINMAX ? K2Smem<HEDDLE_F32, HEDDLE_MINMAX>(n, m, kv).total : K2Smem<HEDDLE_F32, HEDDLE_MINPLUS>(n, m, kv).total;
   if (dt == HEDDLE_F64) return sr == HEDDLE_MINMAX ? K2Smem<HEDDLE_F64, HEDDLE_MINMAX>(n, m, kv).total : K2Smem<HEDDLE_F64, HEDDLE_MINPLUS>(n, m, kv).total;
   return sr == HEDDLE_MINMAX ? K2Smem<HEDDLE_U32, HEDDLE_MINMAX>(n, m, kv).total : K2Smem<HEDDLE_U32, HEDDLE_MINPLUS>(n, m, kv).total;
+}
+
+template <int DT, int SR>
+int fill_launch(const SolveArgs& a, int64_t cells, int grid, cudaStream_t s) {
+  k3_fill<DT, SR><<<grid, 256, 0, s>>>(a, cells);
+  return 0;
+}
+template <int DT, int SR>
+int klo_launch(const SolveArgs& a, int j, int32_t* klo, dim3 g, cudaStream_t s) {
+  k3_klo<DT><<<g, 256, 0, s>>>(a, j, klo);
+  return 0;
+}
+template <int DT, int SR>
+int unpack_launch(const SolveArgs& a, int j, unsigned long long* keys, dim3 g, cudaStream_t s) {
+  k3_unpack<DT, SR><<<g, 256, 0, s>>>(a, j, keys);
+  return 0;
+}
+template <int DT, int SR>
+int finalize_launch(const SolveArgs& a, cudaStream_t s) {
+  k3_finalize<DT, SR><<<(a.B + 255) / 256, 256, 0, s>>>(a);
+  return 0;
 }
 
 template <class V>
@@ -127,6 +177,81 @@ bool check_profile(const heddle_place_config* c, double* gmax) {
     if (g > *gmax) *gmax = g;
   }
   return true;
+}
+
+
+// Batched (one CTA per problem) vs layered (all SMs per layer) -- rough cost model:
+// batched: waves x per-problem cells / (~12 cells/clk for one 4-warp CTA);
+// layered: all cells / (~30 cells/clk/SM x SMs) + per-layer launch/drain (~6000 clk).
+bool use_layered(const heddle_place_ctx* x, int n, int m, int B) {
+  const double cells = (double)heddle_place_transitions(n, m);
+  const double slots = (double)x->num_sms * 8.0;
+  const double waves = std::ceil((double)B / slots);
+  const double t2 = waves * cells / 12.0;
+  const double t3 = (double)B * cells / (30.0 * x->num_sms) + (double)(m - 1) * 6000.0;
+  return t3 < t2;
+}
+
+heddle_status solve_layered(heddle_place_ctx* x, SolveArgs& a, bool kp, bool kv, cudaStream_t s) {
+  const int dt = x->dtype, sr = x->semiring;
+  const int n = a.n, m = a.m, B = a.B;
+  // workspace of the layered path (allocated on first use)
+  if (kv && !x->d_klo) {
+    if (cudaMalloc(&x->d_klo, 4 * (size_t)x->max_batch * (x->max_n + 1)) != cudaSuccess) { cudaGetLastError(); return HEDDLE_E_NOMEM; }
+  }
+  if (kp && !x->d_keys) {
+    if (cudaMalloc(&x->d_keys, 8 * (size_t)x->max_batch * (x->max_n + 1)) != cudaSuccess) { cudaGetLastError(); return HEDDLE_E_NOMEM; }
+    if (cudaMemsetAsync(x->d_keys, 0xff, 8 * (size_t)x->max_batch * (x->max_n + 1), s) != cudaSuccess) return HEDDLE_E_CUDA;
+  }
+  const int64_t cells = (int64_t)B * (m + 1) * (n + 1);
+  const int fill_grid = (int)std::min<int64_t>((cells + 255) / 256, (int64_t)x->num_sms * 16);
+  HP_DISPATCH(fill_launch, a, cells, fill_grid, s);
+  pro_for(dt, sr, kp, kv)<<<B, 256, 0, s>>>(a);
+  x->launches += 2;
+  // tile geometry: 256 columns x kc splits; kc sized for >= ~4 tiles per resident CTA
+  const double layer_cells = (double)B * (double)(n - m + 1) * (double)(n - m + 2) / 2.0;
+  K3Fn fn = k3_for(dt, sr, kp, kv);
+  int kc = 4096;
+  int occ = 0;
+  for (;;) {
+    const int sm = k3_smem(dt, sr, kc);
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kK3Threads, sm);
+    const double tiles = layer_cells / ((double)kK3Cols * kc);
+    if (kc <= 256 || tiles >= 4.0 * occ * x->num_sms) break;
+    kc /= 2;
+  }
+  if (occ < 1) return HEDDLE_E_CUDA;
+  const int smem = k3_smem(dt, sr, kc);
+  LayerArgs la{};
+  la.a = a;
+  la.kc = kc;
+  la.ncb = (n - m + 3) / kK3Cols + 1;
+  la.nq = (n + 3) / kc + 1;
+  la.blk_lo = 0;
+  la.blk_hi = la.ncb;
+  la.klo = kv ? x->d_klo : nullptr;
+  la.keys = kp ? x->d_keys : nullptr;
+  const int64_t ntiles = (int64_t)B * la.ncb * la.nq;
+  const int grid = (int)std::min<int64_t>(ntiles, (int64_t)occ * x->num_sms);
+  for (int j = 2; j <= m; ++j) {
+    la.j = j;
+    if (kv) {
+      dim3 g((n + 256) / 256, B);
+      HP_DISPATCH(klo_launch, a, j, x->d_klo, g, s);
+      x->launches++;
+    }
+    fn<<<grid, kK3Threads, smem, s>>>(la);
+    x->launches++;
+    if (kp) {
+      dim3 g((n + 256) / 256, B);
+      HP_DISPATCH(unpack_launch, a, j, x->d_keys, g, s);
+      x->launches++;
+    }
+  }
+  HP_DISPATCH(finalize_launch, a, s);
+  x->launches++;
+  return cudaGetLastError() == cudaSuccess ? HEDDLE_OK : HEDDLE_E_CUDA;
 }
 
 }  // namespace
@@ -168,6 +293,8 @@ void heddle_place_destroy(heddle_place_ctx* ctx) {
   cudaFree(ctx->d_sp);
   cudaFree(ctx->d_status);
   cudaFree(ctx->d_stage);
+  cudaFree(ctx->d_klo);
+  cudaFree(ctx->d_keys);
   delete ctx;
 }
 
@@ -223,6 +350,7 @@ heddle_status heddle_place_init(const heddle_place_config* c, heddle_place_ctx**
   x->gstride = c->max_n + 1;
   x->lmax_u32 = lmax;
   cudaDeviceGetAttribute(&x->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device);
+  cudaDeviceGetAttribute(&x->num_sms, cudaDevAttrMultiProcessorCount, c->device);
 
   const size_t es = elem_size(c->dtype);
   const size_t des = dp_elem_size(c->dtype, c->semiring);
@@ -287,8 +415,15 @@ heddle_status heddle_place_solve(heddle_place_ctx* x, const heddle_place_problem
     return HEDDLE_E_INVALID;
   const bool kv = p->kv_caps != nullptr;
   const bool kp = (x->flags & HEDDLE_KEEP_PARENTS) != 0;
-  const int smem = k2_smem(x->dtype, x->semiring, p->n, p->m, kv);
-  if (smem > x->k2_smem_max) return HEDDLE_E_INVALID;   // n too large for the one-CTA-per-problem kernel
+  const int smem2 = k2_smem(x->dtype, x->semiring, p->n, p->m, kv);
+  const bool k2_fits = smem2 <= x->k2_smem_max;
+  const bool wide = (x->dtype == HEDDLE_F64) || (x->dtype == HEDDLE_U32 && x->semiring == HEDDLE_MINPLUS);
+  bool layered;
+  if (x->flags & HEDDLE_FORCE_BATCHED) layered = false;
+  else if (x->flags & HEDDLE_FORCE_LAYERED) layered = true;
+  else layered = !k2_fits || use_layered(x, p->n, p->m, p->B);
+  if (!layered && !k2_fits) return HEDDLE_E_INVALID;   // n too large for the one-CTA-per-problem kernel
+  if (layered && kp && wide) return HEDDLE_E_INVALID;    // packed (value, split) atomics need 32-bit values
   DeviceGuard guard(x->device);
   SolveArgs a{};
   a.n = p->n;
@@ -314,11 +449,17 @@ heddle_status heddle_place_solve(heddle_place_ctx* x, const heddle_place_problem
   a.status_out = status_out;
   a.objective = objective_out;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  k2_for(x->dtype, x->semiring, kp, kv)<<<p->B, kK2Threads, smem, s>>>(a);
-  x->launches++;
-  if (cudaGetLastError() != cudaSuccess) return HEDDLE_E_CUDA;
+  if (!layered) {
+    k2_for(x->dtype, x->semiring, kp, kv)<<<p->B, kK2Threads, smem2, s>>>(a);
+    x->launches++;
+    if (cudaGetLastError() != cudaSuccess) return HEDDLE_E_CUDA;
+  } else {
+    const heddle_status st = solve_layered(x, a, kp, kv, s);
+    if (st != HEDDLE_OK) return st;
+  }
   x->last = a;
   x->last_kv = kv;
+  x->last_layered = layered;
   x->solved = true;
   return HEDDLE_OK;
 }

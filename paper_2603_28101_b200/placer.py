@@ -45,7 +45,7 @@ class Placer:
     """One heddle_place context: a profile (MP degrees, T, F) and workspace limits."""
 
     def __init__(self, degrees, T, F, *, dtype="f32", semiring="minmax", max_n, max_m, max_batch,
-                 device=None, keep_parents=False):
+                 device=None, keep_parents=False, kernel="auto"):
         self.dtype = C.DTYPES[dtype] if isinstance(dtype, str) else dtype
         self.semiring = C.SEMIRINGS[semiring] if isinstance(semiring, str) else semiring
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
@@ -58,7 +58,7 @@ class Placer:
         self._F = np.ascontiguousarray(F.astype(npdt))
         cfg = C.Config(self.device.index, self.dtype, self.semiring, max_n, max_m, max_batch, self._deg.size,
                        self._deg.ctypes.data, self._T.ctypes.data, self._F.ctypes.data, self._F.shape[1],
-                       C.KEEP_PARENTS if keep_parents else 0)
+                       (C.KEEP_PARENTS if keep_parents else 0) | C.KERNELS[kernel])
         h = ctypes.c_void_p()
         C.check(C.lib().heddle_place_init(ctypes.byref(cfg), ctypes.byref(h)), "heddle_place_init")
         self._h = h

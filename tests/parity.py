@@ -27,11 +27,12 @@ def to_dev(a, dt=None):
     return t.cuda()
 
 
-def run_gpu(batch, semiring="minmax", keep_parents=False, dtype=None, placer=None, lengths_shared=False):
+def run_gpu(batch, semiring="minmax", keep_parents=False, dtype=None, placer=None, lengths_shared=False,
+            kernel="auto"):
     dtype = dtype or batch.profile.dtype
     if placer is None:
         placer = Placer(batch.profile.degrees, batch.profile.T, batch.profile.F, dtype=dtype, semiring=semiring,
-                        max_n=batch.n, max_m=batch.m, max_batch=batch.B, keep_parents=keep_parents)
+                        max_n=batch.n, max_m=batch.m, max_batch=batch.B, keep_parents=keep_parents, kernel=kernel)
     L = to_dev(batch.lengths[:1] if lengths_shared else batch.lengths, TDT[dtype])
     if lengths_shared:
         L = L[0]

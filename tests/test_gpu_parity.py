@@ -11,6 +11,7 @@ import torch
 import oracle
 from inputs import workloads as wl
 from tests.parity import assert_exact, assert_f64_tolerance, run_gpu, to_dev
+from tests.parity import run_gpu as _run
 
 pytestmark = pytest.mark.gpu
 
@@ -40,25 +41,31 @@ def test_tiny_config_bruteforce(semiring):
             assert np.array_equal(got, cp["parent"][j, j:n - m + j + 1]), (prob, j)
 
 
+KERNELS = ["batched", "layered"]
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("semiring", ["minmax", "minplus"])
 @pytest.mark.parametrize("dtype", ["u32", "f32"])
-def test_random_tiny_exact(dtype, semiring):
+def test_random_tiny_exact(dtype, semiring, kernel):
     """Heavy ties, clamp plateaus, caps, kv caps, heterogeneous degrees: bit-exact."""
     sr = oracle.MINMAX if semiring == "minmax" else oracle.MINPLUS
     for s in range(150):
         batch = wl.tiny_random(s, n_max=20, m_max=6, allow_caps=True, allow_kv=True, dtype=dtype)
-        gpu = run_gpu(batch, semiring=semiring, keep_parents=(s % 2 == 0))
+        kp = (s % 2 == 0) and not (kernel == "layered" and dtype == "u32" and semiring == "minplus")
+        gpu = run_gpu(batch, semiring=semiring, keep_parents=kp, kernel=kernel)
         ref = oracle.solve(oracle.Problem.from_batch(batch, 0, mode=dtype, semiring=sr), want_tables=True)
-        assert_exact(gpu, 0, ref, batch, dtype, semiring, check_parents=(s % 2 == 0), tag=f"{dtype}{s}")
+        assert_exact(gpu, 0, ref, batch, dtype, semiring, check_parents=kp, tag=f"{dtype}{s}")
         gpu["placer"].close()
 
 
+@pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("semiring", ["minmax", "minplus"])
-def test_random_tiny_f64(semiring):
+def test_random_tiny_f64(semiring, kernel):
     sr = oracle.MINMAX if semiring == "minmax" else oracle.MINPLUS
     for s in range(80):
         batch = wl.tiny_random(s, n_max=20, m_max=6, allow_caps=True, allow_kv=True, dtype="f64")
-        gpu = run_gpu(batch, semiring=semiring)
+        gpu = run_gpu(batch, semiring=semiring, kernel=kernel)
         p = oracle.Problem.from_batch(batch, 0, mode="f64", semiring=sr)
         ref = oracle.solve(p)
         if ref["status"] != oracle.OK:
@@ -70,34 +77,37 @@ def test_random_tiny_f64(semiring):
 
 
 # ------------------------------------------------------------------ configs[1]: rollout, FP32
+@pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("semiring", ["minmax", "minplus"])
-def test_rollout_config(semiring):
+def test_rollout_config(semiring, kernel):
     sr = oracle.MINMAX if semiring == "minmax" else oracle.MINPLUS
     for prob in range(4):
         batch = wl.config_rollout(problem=prob)
-        gpu = run_gpu(batch, semiring=semiring, keep_parents=True)
+        gpu = run_gpu(batch, semiring=semiring, keep_parents=True, kernel=kernel)
         ref = oracle.solve(oracle.Problem.from_batch(batch, 0, mode="f32", semiring=sr), want_tables=True)
         assert_exact(gpu, 0, ref, batch, "f32", semiring, check_parents=True, tag=f"rollout{prob}")
         p64 = oracle.Problem.from_batch(batch, 0, mode="f64", semiring=sr)
         assert_f64_tolerance(gpu["obj"][0], gpu["bounds"][0], p64, semiring, tag=f"rollout{prob}")
 
 
-def test_rollout_with_caps_and_kv():
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_rollout_with_caps_and_kv(kernel):
     """Worker batch caps (max_active) and KV token caps on the rollout workload."""
     batch = wl.config_rollout(problem=7)
     rng = np.random.default_rng(11)
     batch.caps = rng.integers(16, 40, size=(1, batch.m)).astype(np.int32)
     total = float(batch.lengths.astype(np.float64).sum())
     batch.kv_caps = rng.integers(int(total / 20), int(total / 8), size=(1, batch.m)).astype(np.int64)
-    gpu = run_gpu(batch, keep_parents=True)
+    gpu = run_gpu(batch, keep_parents=True, kernel=kernel)
     ref = oracle.solve(oracle.Problem.from_batch(batch, 0, mode="f32"), want_tables=True)
     assert_exact(gpu, 0, ref, batch, "f32", "minmax", check_parents=True, tag="rollout-caps")
 
 
 # ------------------------------------------------------------------ configs[2]: TP sweep (shared L, stride 0)
-def test_tp_sweep_config():
+@pytest.mark.parametrize("kernel", ["auto", "batched"])
+def test_tp_sweep_config(kernel):
     batch = wl.config_tp_sweep()
-    gpu = run_gpu(batch, lengths_shared=True)
+    gpu = run_gpu(batch, lengths_shared=True, kernel=kernel)
     rows = np.stack([batch.profile.row_of(batch.degrees[b]) for b in range(batch.B)])
     opt, bounds, _ = oracle.solve_batch(batch.lengths, batch.profile.T, batch.profile.F, rows, mode="f32")
     for b in range(batch.B):
@@ -117,9 +127,10 @@ def test_batched_sample_exact():
     assert np.array_equal(gpu["bounds"], bounds)
 
 
-def test_batched_keep_parents():
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_batched_keep_parents(kernel):
     batch = wl.config_batched(B=6, seed_problem=3)
-    gpu = run_gpu(batch, keep_parents=True)
+    gpu = run_gpu(batch, keep_parents=True, kernel=kernel)
     for b in range(batch.B):
         ref = oracle.solve(oracle.Problem.from_batch(batch, b, mode="f32"), want_tables=True)
         assert_exact(gpu, b, ref, batch, "f32", "minmax", check_parents=True, tag=f"batched{b}")
@@ -150,8 +161,10 @@ def _single(L, deg, dtype="f32", m=None, profile=None, caps=None, semiring="minm
     return b
 
 
-def test_edge_cases():
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_edge_cases(kernel):
     f = np.float32
+    run_gpu = lambda b: _run(b, kernel=kernel)
     # n = m = 1
     g = run_gpu(_single(np.array([100], f), [1]))
     assert g["status"][0] == 0 and list(g["bounds"][0]) == [0, 1]
@@ -182,7 +195,8 @@ def test_edge_cases():
     assert g["status"][0] == 4
 
 
-def test_ragged_sizes_and_mixed_batch():
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_ragged_sizes_and_mixed_batch(kernel):
     """n not a multiple of 4 or of the 128-column warp block; one bad problem in a batch
     does not disturb the others."""
     for n, m in [(129, 3), (130, 7), (257, 2), (383, 31), (1021, 5)]:
@@ -192,7 +206,7 @@ def test_ragged_sizes_and_mixed_batch():
         L[1, 3], L[1, 4] = L[1, 4], L[1, 3] + 1000   # problem 1 unsorted
         deg = wl.sorted_degree_vectors(rng, 3, m)
         batch = wl.Batch("ragged", n, m, L.astype(np.float32), deg, wl.float_profile())
-        gpu = run_gpu(batch, keep_parents=True)
+        gpu = run_gpu(batch, keep_parents=True, kernel=kernel)
         assert gpu["status"][1] == 2
         for b in (0, 2):
             ref = oracle.solve(oracle.Problem.from_batch(batch, b, mode="f32"), want_tables=True)
@@ -229,3 +243,34 @@ def test_error_paths():
     with pytest.raises(HeddleError) as e:   # parents without HEDDLE_KEEP_PARENTS
         pl.backtrack(parents=True)
     assert e.value.status == E_STATE
+
+
+# ------------------------------------------------------------------ layered kernel at larger n
+def test_layered_medium_exact():
+    """n = 8192 (beyond nothing for K2 but exercised through K3), m = 16, vs the full oracle."""
+    rng = np.random.default_rng(77)
+    n, m = 8192, 16
+    L = wl.presort(wl.predicted(rng, wl.coding_lengths(rng, n // 8, 8)))
+    deg = wl.sorted_degree_vectors(rng, 2, m)
+    batch = wl.Batch("medium", n, m, np.stack([L, L]).astype(np.float32), deg, wl.float_profile())
+    gpu = run_gpu(batch, kernel="layered")
+    rows = np.stack([batch.profile.row_of(batch.degrees[b]) for b in range(batch.B)])
+    opt, bounds, _ = oracle.solve_batch(batch.lengths, batch.profile.T, batch.profile.F, rows, mode="f32",
+                                        threads=2)
+    assert np.array_equal(gpu["obj"], opt)
+    assert np.array_equal(gpu["bounds"], bounds)
+
+
+def test_large_config_objective_parametric():
+    """configs[4]: n = 65536, m = 256 on one GPU (layered kernel).  The objective is pinned
+    exactly by the parametric oracle (P6); the partition must attain it group by group."""
+    batch = wl.config_large()
+    gpu = run_gpu(batch)
+    assert gpu["status"][0] == 0
+    p = oracle.Problem.from_batch(batch, 0, mode="f32")
+    q = oracle.parametric_opt(p)
+    assert gpu["obj"][0] == q["opt"], (gpu["obj"][0], q["opt"])
+    bd = gpu["bounds"][0]
+    assert bd[0] == 0 and bd[-1] == batch.n and np.all(np.diff(bd) > 0)
+    worst = max(oracle.group_cost(p, j, int(bd[j - 1]), int(bd[j])) for j in range(1, batch.m + 1))
+    assert worst == q["opt"]
