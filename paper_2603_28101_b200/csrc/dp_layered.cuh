@@ -2,9 +2,9 @@
 // the layer's (column, split) triangle cut into uniform tiles spread over every SM.
 //
 // Same recurrence and arithmetic as K2 (Eq. 3; traits.cuh).  A tile is
-// (problem b, 256 consecutive columns, a chunk of KC splits); the CTA stages
+// (problem b, 512 consecutive columns, a chunk of KC splits); the CTA stages
 // dp[j-1][k0..k1), L[k0..k1) and the G window it needs (plus the one-element
-// shifted copy for the FMUL2 column pairs) in shared memory, its 4 warps run the K2
+// shifted copy for the FMUL2 column pairs) in shared memory, its 8 warps run the K2
 // sliding sweep (64 columns each, 4 split quarters), and the per-column partial
 // minima of the chunk are merged into dp[j][i] with atomicMin on the value's bit
 // pattern (all values are non-negative, so the unsigned order is the value order;
@@ -17,9 +17,9 @@
 
 namespace hp {
 
-constexpr int kK3Warps = 4;
+constexpr int kK3Warps = 8;
 constexpr int kK3Threads = 32 * kK3Warps;
-constexpr int kK3Cols = kK3Warps * kWarpCols;   // 256 columns per tile
+constexpr int kK3Cols = kK3Warps * kWarpCols;   // 512 columns per tile
 constexpr int kK3GPadLo = 23;                    // == 3 (mod 4): G staging below c0 - k1
 constexpr int kK3LPad = 24;
 

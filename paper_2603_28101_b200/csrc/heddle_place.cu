@@ -211,7 +211,7 @@ heddle_status solve_layered(heddle_place_ctx* x, SolveArgs& a, bool kp, bool kv,
   // tile geometry: 256 columns x kc splits; kc sized for >= ~4 tiles per resident CTA
   const double layer_cells = (double)B * (double)(n - m + 1) * (double)(n - m + 2) / 2.0;
   K3Fn fn = k3_for(dt, sr, kp, kv);
-  int kc = 4096;
+  int kc = 2048;
   int occ = 0;
   for (;;) {
     const int sm = k3_smem(dt, sr, kc);
