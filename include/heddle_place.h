@@ -161,6 +161,29 @@ int64_t heddle_place_launch_count(const heddle_place_ctx* ctx);
  * W = 2(n-m+1) + (m-2)(n-m+1)(n-m+2)/2 for m >= 2, W(n,1) = 1, 0 if n < m. */
 int64_t heddle_place_transitions(int32_t n, int32_t m);
 
+/* ---- multi-GPU split mode (one large instance) -------------------------
+ * The columns of every DP layer are dealt to `world` ranks in zigzag order of
+ * 512-column blocks (rank r owns blocks r and 2P-1-r of every group of 2P, which
+ * balances the triangular work); each rank computes its blocks with the layered
+ * kernel and the finished row is exchanged with one ncclAllGather per layer on the
+ * solve stream.  Every rank then holds every dp row, so objective and boundaries
+ * are identical on all ranks (and bit-identical to a single-GPU solve).
+ * heddle_place_solve / _backtrack are collective: all ranks call them with the same
+ * problem.  HEDDLE_KEEP_PARENTS is not available in split mode (E_INVALID).
+ *
+ * heddle_place_nccl_unique_id: fills `bytes` >= 128 bytes (an ncclUniqueId) on one
+ *   rank; the caller broadcasts it (e.g. torch.distributed) to every rank.
+ * heddle_place_init_split: like heddle_place_init on cfg->device, plus
+ *   ncclCommInitRank(world, id, rank).  nccl_unique_id == NULL with rank 0 selects
+ *   the single-device EMULATION (all virtual ranks computed on this GPU, exchange
+ *   by copy) used to test the ownership / packing logic without NCCL.
+ * heddle_place_split_blocks: host-only; writes the column blocks rank owns out of
+ *   ncb (up to cap entries) and returns how many it owns (-1 on bad arguments). */
+heddle_status heddle_place_nccl_unique_id(void* id_out, int32_t bytes);
+heddle_status heddle_place_init_split(const heddle_place_config* cfg, const void* nccl_unique_id, int32_t rank,
+                                      int32_t world, heddle_place_ctx** out);
+int32_t heddle_place_split_blocks(int32_t ncb, int32_t world, int32_t rank, int32_t* blocks_out, int32_t cap);
+
 void heddle_place_destroy(heddle_place_ctx* ctx);
 const char* heddle_place_strerror(heddle_status s);
 

@@ -15,6 +15,20 @@ LIB = os.path.join(PKG, "libheddle_place.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _nccl_dir():
+    try:
+        import nvidia.nccl
+        return os.path.dirname(nvidia.nccl.__file__) if nvidia.nccl.__file__ else list(nvidia.nccl.__path__)[0]
+    except Exception:
+        return os.path.join(sys.prefix, "lib", f"python{sys.version_info.major}.{sys.version_info.minor}",
+                            "site-packages", "nvidia", "nccl")
+
+
+NCCL = _nccl_dir()
+NCCL_FLAGS = ["-I", os.path.join(NCCL, "include"), "-L", os.path.join(NCCL, "lib"), "-l:libnccl.so.2",
+              "-Xlinker", "-rpath=" + os.path.join(NCCL, "lib")]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC,-O2",
          "-Xptxas", "-warn-spills", "-cudart", "shared"]
 
@@ -50,7 +64,7 @@ def stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
-    cmd = [NVCC, *ARCH, *FLAGS, "-I", INCLUDE, "-shared", "-o", LIB, *sources()]
+    cmd = [NVCC, *ARCH, *FLAGS, "-I", INCLUDE, "-shared", "-o", LIB, *sources(), *NCCL_FLAGS]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)

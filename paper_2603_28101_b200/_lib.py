@@ -26,7 +26,8 @@ SEMIRINGS = {"minmax": MINMAX, "minplus": MINPLUS}
 # exported symbols declared in include/heddle_place.h (tests check the .so exports all of them)
 SYMBOLS = ("heddle_place_init", "heddle_place_solve", "heddle_place_backtrack", "heddle_place_solve_host",
            "heddle_place_launch_count", "heddle_place_transitions", "heddle_place_destroy",
-           "heddle_place_strerror")
+           "heddle_place_strerror", "heddle_place_nccl_unique_id", "heddle_place_init_split",
+           "heddle_place_split_blocks")
 
 
 class Config(ctypes.Structure):
@@ -78,6 +79,13 @@ def lib() -> ctypes.CDLL:
         L.heddle_place_transitions.restype = ctypes.c_int64
         L.heddle_place_destroy.argtypes = [vp]
         L.heddle_place_destroy.restype = None
+        L.heddle_place_nccl_unique_id.argtypes = [vp, ctypes.c_int32]
+        L.heddle_place_nccl_unique_id.restype = ctypes.c_int
+        L.heddle_place_init_split.argtypes = [ctypes.POINTER(Config), vp, ctypes.c_int32, ctypes.c_int32,
+                                              ctypes.POINTER(vp)]
+        L.heddle_place_init_split.restype = ctypes.c_int
+        L.heddle_place_split_blocks.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, vp, ctypes.c_int32]
+        L.heddle_place_split_blocks.restype = ctypes.c_int32
         L.heddle_place_strerror.argtypes = [ctypes.c_int]
         L.heddle_place_strerror.restype = ctypes.c_char_p
         _lib = L
@@ -96,3 +104,19 @@ def transitions(n: int, m: int) -> int:
 def check(status: int, what: str):
     if status != OK:
         raise HeddleError(status, what)
+
+
+def split_blocks(ncb: int, world: int, rank: int) -> list[int]:
+    """Column blocks (512 columns each) that `rank` computes in split mode (zigzag ownership)."""
+    cnt = lib().heddle_place_split_blocks(ncb, world, rank, None, 0)
+    if cnt < 0:
+        raise ValueError("bad split arguments")
+    buf = (ctypes.c_int32 * max(cnt, 1))()
+    lib().heddle_place_split_blocks(ncb, world, rank, buf, cnt)
+    return list(buf[:cnt])
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    check(lib().heddle_place_nccl_unique_id(buf, 128), "heddle_place_nccl_unique_id")
+    return buf.raw

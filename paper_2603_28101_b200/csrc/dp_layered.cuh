@@ -29,8 +29,8 @@ struct LayerArgs {
   int kc;           // splits per tile (multiple of 16)
   int ncb;          // column blocks per problem
   int nq;           // split chunks per column block (max)
-  int blk_lo, blk_hi;   // column blocks [blk_lo, blk_hi) owned by this launch (split mode), else [0, ncb)
-  int blk_stride;   // block ownership: block b owned iff (b in [blk_lo, blk_hi)) -- contiguous
+  int own_rank, own_world;   // split mode: compute only the column blocks zigzag-owned by own_rank
+  int nown;                  // owned-block slots per rank (ncb when own_world == 1)
   const int32_t* klo;   // [B][n+1] kv lower bounds for this layer, or null
   unsigned long long* keys;   // [B][n+1] packed (value, split) minima (KEEP_PARENTS), or null
 };
@@ -156,6 +156,66 @@ __global__ void k3_klo(SolveArgs a, int j, int32_t* klo) {
   }
 }
 
+// ---------------------------------------------------------------- split-mode column ownership
+// Column blocks (kK3Cols wide, from cbase = j & ~3) are dealt to P ranks in zigzag
+// order: in every group of 2P consecutive blocks rank r owns blocks r and 2P-1-r, so
+// the triangular work of each pair sums to a constant (a contiguous split would leave
+// the last rank 23% of the triangle at P = 8).  Slot s of rank r is its s-th block.
+__host__ __device__ inline int owned_block(int slot, int rank, int world) {
+  if (world <= 1) return slot;
+  const int g = slot >> 1;
+  return 2 * world * g + ((slot & 1) ? (2 * world - 1 - rank) : rank);
+}
+__host__ __device__ inline int owned_slots(int ncb, int world) {
+  return world <= 1 ? ncb : 2 * ((ncb + 2 * world - 1) / (2 * world));
+}
+
+// pack row j of the blocks owned by `rank` into buf[b][slot][kK3Cols] (+inf padding)
+template <int DT, int SR>
+__global__ void k3_pack(SolveArgs a, int j, int rank, int world, int nown, void* buf) {
+  using T = Tr<DT, SR>;
+  using D = typename T::D;
+  const int n = a.n, m = a.m, b = blockIdx.y;
+  const int cbase = j & ~3;
+  const D* row = reinterpret_cast<const D*>(a.dpws) + ((int64_t)b * (m + 1) + j) * (n + 1);
+  D* out = reinterpret_cast<D*>(buf) + (int64_t)b * nown * kK3Cols;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nown * kK3Cols; t += gridDim.x * blockDim.x) {
+    const int i = cbase + kK3Cols * owned_block(t / kK3Cols, rank, world) + (t % kK3Cols);
+    out[t] = (i <= n) ? row[i] : T::inf();
+  }
+}
+
+// scatter an all-gathered buffer recv[rank][b][slot][kK3Cols] into row j of every rank's blocks
+template <int DT, int SR>
+__global__ void k3_unpack_rows(SolveArgs a, int j, int world, int nown, const void* recv) {
+  using T = Tr<DT, SR>;
+  using D = typename T::D;
+  const int n = a.n, m = a.m, b = blockIdx.y;
+  const int cbase = j & ~3;
+  const int imax = n - m + j;
+  D* row = reinterpret_cast<D*>(a.dpws) + ((int64_t)b * (m + 1) + j) * (n + 1);
+  const D* in = reinterpret_cast<const D*>(recv);
+  const int64_t per_rank = (int64_t)a.B * nown * kK3Cols;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)world * nown * kK3Cols;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(t / ((int64_t)nown * kK3Cols));
+    const int rem = (int)(t % ((int64_t)nown * kK3Cols));
+    const int i = cbase + kK3Cols * owned_block(rem / kK3Cols, r, world) + (rem % kK3Cols);
+    if (i >= j && i <= imax) row[i] = in[r * per_rank + (int64_t)b * nown * kK3Cols + rem];
+  }
+}
+
+// clear the computed region of row j to +inf (split emulation: row rebuilt from the exchange)
+template <int DT, int SR>
+__global__ void k3_row_fill(SolveArgs a, int j) {
+  using T = Tr<DT, SR>;
+  using D = typename T::D;
+  const int n = a.n, m = a.m, b = blockIdx.y;
+  D* row = reinterpret_cast<D*>(a.dpws) + ((int64_t)b * (m + 1) + j) * (n + 1);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += gridDim.x * blockDim.x)
+    if (i >= j && i <= n - m + j) row[i] = T::inf();
+}
+
 // ---------------------------------------------------------------- one layer, tiled
 template <int DT, int SR>
 struct K3Smem {
@@ -192,11 +252,11 @@ __global__ void __launch_bounds__(kK3Threads) k3_layer(LayerArgs la) {
   const int imax_layer = n - m + j;
   const int cbase = j & ~3;
   const int kstart = (j - 1) & ~3;
-  const int nblk = la.blk_hi - la.blk_lo;
+  const int nblk = la.nown;
   const int64_t ntiles = (int64_t)a.B * nblk * la.nq;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int q = (int)(tile % la.nq);
-    const int blk = la.blk_lo + (int)((tile / la.nq) % nblk);
+    const int blk = owned_block((int)((tile / la.nq) % nblk), la.own_rank, la.own_world);
     const int b = (int)(tile / ((int64_t)la.nq * nblk));
     const int c0 = cbase + kK3Cols * blk;
     if (c0 > imax_layer) continue;                              // (uniform across the CTA)

@@ -3,6 +3,7 @@
 // dispatch.  Device side: K1 cost tables (this file), K2 batched DP
 // (dp_batched.cuh), K4 backtrack (backtrack.cuh).
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <cmath>
 #include <cstdint>
@@ -64,6 +65,13 @@ struct heddle_place_ctx {
   int32_t* d_klo = nullptr;             // [max_batch][max_n+1] (layered kernel, kv caps)
   unsigned long long* d_keys = nullptr; // [max_batch][max_n+1] (layered kernel, KEEP_PARENTS)
   bool last_layered = false;
+  // split mode (one large instance over several GPUs)
+  int split_rank = 0, split_world = 1;
+  bool split_emulate = false;           // all virtual ranks on this device, exchange by copy (tests)
+  ncclComm_t comm = nullptr;
+  void* d_send = nullptr;
+  void* d_recv = nullptr;
+  size_t xbuf_bytes = 0;
 };
 
 namespace {
@@ -155,6 +163,21 @@ int unpack_launch(const SolveArgs& a, int j, unsigned long long* keys, dim3 g, c
   return 0;
 }
 template <int DT, int SR>
+int pack_launch(const SolveArgs& a, int j, int rank, int world, int nown, void* buf, dim3 g, cudaStream_t s) {
+  k3_pack<DT, SR><<<g, 256, 0, s>>>(a, j, rank, world, nown, buf);
+  return 0;
+}
+template <int DT, int SR>
+int unpack_rows_launch(const SolveArgs& a, int j, int world, int nown, const void* recv, dim3 g, cudaStream_t s) {
+  k3_unpack_rows<DT, SR><<<g, 256, 0, s>>>(a, j, world, nown, recv);
+  return 0;
+}
+template <int DT, int SR>
+int row_fill_launch(const SolveArgs& a, int j, dim3 g, cudaStream_t s) {
+  k3_row_fill<DT, SR><<<g, 256, 0, s>>>(a, j);
+  return 0;
+}
+template <int DT, int SR>
 int finalize_launch(const SolveArgs& a, cudaStream_t s) {
   k3_finalize<DT, SR><<<(a.B + 255) / 256, 256, 0, s>>>(a);
   return 0;
@@ -228,12 +251,32 @@ heddle_status solve_layered(heddle_place_ctx* x, SolveArgs& a, bool kp, bool kv,
   la.kc = kc;
   la.ncb = (n - m + 3) / kK3Cols + 1;
   la.nq = (n + 3) / kc + 1;
-  la.blk_lo = 0;
-  la.blk_hi = la.ncb;
+  const int world = x->split_world;
+  la.own_world = world;
+  la.own_rank = x->split_rank;
+  la.nown = owned_slots(la.ncb, world);
   la.klo = kv ? x->d_klo : nullptr;
   la.keys = kp ? x->d_keys : nullptr;
-  const int64_t ntiles = (int64_t)B * la.ncb * la.nq;
+  const int64_t ntiles = (int64_t)B * la.nown * la.nq;
   const int grid = (int)std::min<int64_t>(ntiles, (int64_t)occ * x->num_sms);
+  // split-mode exchange buffers: send [B][nown][kK3Cols], recv [world][B][nown][kK3Cols]
+  const size_t des = dp_elem_size(dt, sr);
+  const size_t slab = (size_t)B * la.nown * kK3Cols;
+  if (world > 1 && x->xbuf_bytes < slab * des) {
+    cudaFree(x->d_send);
+    cudaFree(x->d_recv);
+    x->d_send = x->d_recv = nullptr;
+    x->xbuf_bytes = 0;
+    if (cudaMalloc(&x->d_send, slab * des) != cudaSuccess || cudaMalloc(&x->d_recv, slab * des * world) != cudaSuccess) {
+      cudaGetLastError();
+      return HEDDLE_E_NOMEM;
+    }
+    x->xbuf_bytes = slab * des;
+  }
+  const ncclDataType_t nt = dt == HEDDLE_F32 ? ncclFloat32 : dt == HEDDLE_F64 ? ncclFloat64
+                            : (sr == HEDDLE_MINMAX ? ncclUint32 : ncclUint64);
+  const dim3 pg((unsigned)std::min<int64_t>((slab / B + 255) / 256, 1024), B);
+  const dim3 ug((unsigned)std::min<int64_t>((slab * world / B + 255) / 256, 2048), B);
   for (int j = 2; j <= m; ++j) {
     la.j = j;
     if (kv) {
@@ -241,8 +284,31 @@ heddle_status solve_layered(heddle_place_ctx* x, SolveArgs& a, bool kp, bool kv,
       HP_DISPATCH(klo_launch, a, j, x->d_klo, g, s);
       x->launches++;
     }
-    fn<<<grid, kK3Threads, smem, s>>>(la);
-    x->launches++;
+    if (world > 1 && x->split_emulate) {
+      // every virtual rank computes its blocks; the all-gather is emulated by packing each
+      // rank's blocks into its recv slab, clearing the row and unpacking it again
+      for (int vr = 0; vr < world; ++vr) {
+        la.own_rank = vr;
+        fn<<<grid, kK3Threads, smem, s>>>(la);
+        x->launches++;
+      }
+      for (int vr = 0; vr < world; ++vr) {
+        HP_DISPATCH(pack_launch, a, j, vr, world, la.nown, static_cast<char*>(x->d_recv) + vr * slab * des, pg, s);
+        x->launches++;
+      }
+      HP_DISPATCH(row_fill_launch, a, j, dim3((n + 256) / 256, B), s);
+      HP_DISPATCH(unpack_rows_launch, a, j, world, la.nown, x->d_recv, ug, s);
+      x->launches += 2;
+    } else {
+      fn<<<grid, kK3Threads, smem, s>>>(la);
+      x->launches++;
+      if (world > 1) {
+        HP_DISPATCH(pack_launch, a, j, x->split_rank, world, la.nown, x->d_send, pg, s);
+        if (ncclAllGather(x->d_send, x->d_recv, slab, nt, x->comm, s) != ncclSuccess) return HEDDLE_E_NCCL;
+        HP_DISPATCH(unpack_rows_launch, a, j, world, la.nown, x->d_recv, ug, s);
+        x->launches += 2;
+      }
+    }
     if (kp) {
       dim3 g((n + 256) / 256, B);
       HP_DISPATCH(unpack_launch, a, j, x->d_keys, g, s);
@@ -295,6 +361,9 @@ void heddle_place_destroy(heddle_place_ctx* ctx) {
   cudaFree(ctx->d_stage);
   cudaFree(ctx->d_klo);
   cudaFree(ctx->d_keys);
+  cudaFree(ctx->d_send);
+  cudaFree(ctx->d_recv);
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
   delete ctx;
 }
 
@@ -419,11 +488,13 @@ heddle_status heddle_place_solve(heddle_place_ctx* x, const heddle_place_problem
   const bool k2_fits = smem2 <= x->k2_smem_max;
   const bool wide = (x->dtype == HEDDLE_F64) || (x->dtype == HEDDLE_U32 && x->semiring == HEDDLE_MINPLUS);
   bool layered;
-  if (x->flags & HEDDLE_FORCE_BATCHED) layered = false;
+  if (x->split_world > 1) layered = true;
+  else if (x->flags & HEDDLE_FORCE_BATCHED) layered = false;
   else if (x->flags & HEDDLE_FORCE_LAYERED) layered = true;
   else layered = !k2_fits || use_layered(x, p->n, p->m, p->B);
   if (!layered && !k2_fits) return HEDDLE_E_INVALID;   // n too large for the one-CTA-per-problem kernel
   if (layered && kp && wide) return HEDDLE_E_INVALID;    // packed (value, split) atomics need 32-bit values
+  if (x->split_world > 1 && (!layered || kp)) return HEDDLE_E_INVALID;  // split mode: layered, no parent table
   DeviceGuard guard(x->device);
   SolveArgs a{};
   a.n = p->n;
@@ -549,6 +620,61 @@ heddle_status heddle_place_solve_host(heddle_place_ctx* x, const heddle_place_pr
   if (bytes_h2d) *bytes_h2d = h2d;
   if (bytes_d2h) *bytes_d2h = d2h;
   return HEDDLE_OK;
+}
+
+
+heddle_status heddle_place_nccl_unique_id(void* id_out, int32_t bytes) {
+  if (!id_out || bytes < (int32_t)sizeof(ncclUniqueId)) return HEDDLE_E_INVALID;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return HEDDLE_E_NCCL;
+  std::memcpy(id_out, &id, sizeof(id));
+  return HEDDLE_OK;
+}
+
+heddle_status heddle_place_init_split(const heddle_place_config* cfg, const void* nccl_unique_id, int32_t rank,
+                                      int32_t world, heddle_place_ctx** out) {
+  if (!out) return HEDDLE_E_INVALID;
+  *out = nullptr;
+  if (world < 1 || rank < 0 || rank >= world || (cfg && (cfg->flags & HEDDLE_KEEP_PARENTS)))
+    return HEDDLE_E_INVALID;
+  if (nccl_unique_id == nullptr && rank != 0) return HEDDLE_E_INVALID;   // emulation: one process
+  heddle_place_config c = *cfg;
+  c.flags |= HEDDLE_FORCE_LAYERED;
+  heddle_place_ctx* x = nullptr;
+  heddle_status st = heddle_place_init(&c, &x);
+  if (st != HEDDLE_OK) return st;
+  x->split_world = world;
+  x->split_rank = rank;
+  if (world > 1) {
+    if (nccl_unique_id == nullptr) {
+      x->split_emulate = true;
+    } else {
+      DeviceGuard guard(x->device);
+      ncclUniqueId id;
+      std::memcpy(&id, nccl_unique_id, sizeof(id));
+      if (ncclCommInitRank(&x->comm, world, id, rank) != ncclSuccess) {
+        x->comm = nullptr;
+        heddle_place_destroy(x);
+        return HEDDLE_E_NCCL;
+      }
+    }
+  }
+  *out = x;
+  return HEDDLE_OK;
+}
+
+int32_t heddle_place_split_blocks(int32_t ncb, int32_t world, int32_t rank, int32_t* blocks_out, int32_t cap) {
+  if (ncb < 0 || world < 1 || rank < 0 || rank >= world) return -1;
+  const int slots = owned_slots(ncb, world);
+  int cnt = 0;
+  for (int sl = 0; sl < slots; ++sl) {
+    const int b = owned_block(sl, rank, world);
+    if (b < ncb) {
+      if (blocks_out && cnt < cap) blocks_out[cnt] = b;
+      ++cnt;
+    }
+  }
+  return cnt;
 }
 
 }  // extern "C"

@@ -49,3 +49,16 @@ def solve_sharded(placer, lengths, degrees, caps=None, kv_caps=None, gather=True
     if not gather or world == 1:
         return obj, bnd, st
     return gather_shards(obj, B, group), gather_shards(bnd, B, group), gather_shards(st, B, group)
+
+
+def split_placer(profile, *, max_n, max_m, max_batch=1, group=None, **kw):
+    """Create a split-mode Placer on this rank's GPU: rank 0 draws the NCCL unique id and
+    broadcasts it over the torch.distributed group; every rank then joins the library's
+    NCCL communicator.  Solves on the returned placer are collective."""
+    from . import _lib as C
+    from .placer import Placer
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    obj = [C.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    return Placer.from_profile(profile, max_n=max_n, max_m=max_m, max_batch=max_batch,
+                               split=(obj[0], rank, world), **kw)

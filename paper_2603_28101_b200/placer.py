@@ -45,7 +45,9 @@ class Placer:
     """One heddle_place context: a profile (MP degrees, T, F) and workspace limits."""
 
     def __init__(self, degrees, T, F, *, dtype="f32", semiring="minmax", max_n, max_m, max_batch,
-                 device=None, keep_parents=False, kernel="auto"):
+                 device=None, keep_parents=False, kernel="auto", split=None):
+        """split=(unique_id_bytes or None, rank, world): multi-GPU split mode (collective solves);
+        unique_id None with rank 0 runs the single-device emulation of `world` ranks."""
         self.dtype = C.DTYPES[dtype] if isinstance(dtype, str) else dtype
         self.semiring = C.SEMIRINGS[semiring] if isinstance(semiring, str) else semiring
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
@@ -60,7 +62,13 @@ class Placer:
                        self._deg.ctypes.data, self._T.ctypes.data, self._F.ctypes.data, self._F.shape[1],
                        (C.KEEP_PARENTS if keep_parents else 0) | C.KERNELS[kernel])
         h = ctypes.c_void_p()
-        C.check(C.lib().heddle_place_init(ctypes.byref(cfg), ctypes.byref(h)), "heddle_place_init")
+        if split is None:
+            C.check(C.lib().heddle_place_init(ctypes.byref(cfg), ctypes.byref(h)), "heddle_place_init")
+        else:
+            uid, rank, world = split
+            idbuf = None if uid is None else ctypes.create_string_buffer(bytes(uid), len(uid))
+            C.check(C.lib().heddle_place_init_split(ctypes.byref(cfg), idbuf, rank, world, ctypes.byref(h)),
+                    "heddle_place_init_split")
         self._h = h
         self.keep_parents = keep_parents
         self.max_n, self.max_m, self.max_batch = max_n, max_m, max_batch

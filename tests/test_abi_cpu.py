@@ -102,3 +102,18 @@ def test_product_path_has_no_oracle_import():
                 src = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src, f
                 assert "heddle_oracle" not in src and "liboracle" not in src, f
+
+
+def test_split_block_ownership(C):
+    """Zigzag ownership: every column block owned by exactly one rank, and the triangular
+    work (block b costs ~ b + 1/2 column-blocks of splits) is balanced across ranks."""
+    for ncb in (1, 3, 16, 128, 129, 255):
+        for world in (1, 2, 3, 4, 8):
+            owned = [C.split_blocks(ncb, world, r) for r in range(world)]
+            allb = sorted(b for o in owned for b in o)
+            assert allb == list(range(ncb)), (ncb, world)
+            if ncb % (2 * world) == 0:
+                work = [sum(b + 0.5 for b in o) for o in owned]
+                assert max(work) == min(work), (ncb, world, work)
+    with pytest.raises(ValueError):
+        C.split_blocks(4, 2, 2)
