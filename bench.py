@@ -180,14 +180,32 @@ def run_cuda(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    lo, hi = shard(B_TOTAL, world, rank)
+    if args.workload == "batched":
+        lo, hi = shard(B_TOTAL, world, rank)
+        batch = wl.config_batched()
+        n_, m_, b_total, workload = N, M, B_TOTAL, WORKLOAD
+        parallelism = f"dp{world} (problems block-sharded, no collective)"
+        kernel_name = "k2_dp_batched<F32,MINMAX>"
+    else:   # configs[4]: one n=65536, m=256 instance, columns split across ranks (NCCL all-gather per layer)
+        batch = wl.config_large()
+        lo, hi = 0, 1
+        n_, m_, b_total = batch.n, batch.m, 1
+        workload = ("single large instance (BASELINE configs[4]): N=65536 coding-like predicted lengths into "
+                    "K=256 workers, FP32, Eq. 3 min-max")
+        parallelism = f"split{world} (zigzag column blocks, per-layer NCCL all-gather of the dp row)"
+        kernel_name = "k3_layer<F32,MINMAX>"
     Bl = hi - lo
-    batch = wl.config_batched()
     L = torch.from_numpy(np.ascontiguousarray(batch.lengths[lo:hi])).to(dev)
     D = torch.from_numpy(np.ascontiguousarray(batch.degrees[lo:hi].astype(np.int32))).to(dev)
     Lh = torch.from_numpy(np.ascontiguousarray(batch.lengths[lo:hi])).pin_memory()
     Dh = torch.from_numpy(np.ascontiguousarray(batch.degrees[lo:hi].astype(np.int32))).pin_memory()
-    placer = Placer.from_profile(batch.profile, max_n=N, max_m=M, max_batch=Bl, device=local)
+    if args.workload == "batched":
+        placer = Placer.from_profile(batch.profile, max_n=n_, max_m=m_, max_batch=Bl, device=local)
+    elif world > 1:
+        from paper_2603_28101_b200.dist import split_placer
+        placer = split_placer(batch.profile, max_n=n_, max_m=m_, max_batch=1)
+    else:
+        placer = Placer.from_profile(batch.profile, max_n=n_, max_m=m_, max_batch=1, device=local, kernel="layered")
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
 
@@ -217,8 +235,8 @@ def run_cuda(args):
         dist.barrier()
     torch.cuda.synchronize()
     t_step = sum(e[0].elapsed_time(e[2]) for e in ev) / 1e3          # seconds, K steps
-    t_k2 = sum(e[0].elapsed_time(e[1]) for e in ev) / 1e3            # dominant kernel: K2 solve
-    W = _lib.transitions(N, M)
+    t_k2 = sum(e[0].elapsed_time(e[1]) for e in ev) / 1e3            # dominant kernel(s): the solve
+    W = _lib.transitions(n_, m_)
 
     # end to end through the public API with host buffers (H2D + solve + backtrack + D2H each step)
     for _ in range(2):
@@ -243,25 +261,26 @@ def run_cuda(args):
         dist.all_reduce(sm, op=dist.ReduceOp.SUM)
         t_step, t_k2, t_e2e = mx[0].item(), mx[1].item(), mx[2].item()
         launches = int(sm[3].item())
-    cells = B_TOTAL * W * args.steps
+    cells = b_total * W * args.steps
     if rank == 0:
         value = cells / t_step
         clocks = clk.summary()
         pk = peaks()
         peak_mhz = pk.get("sm_max_mhz", 1965.0)
-        k2_rate = Bl * W * args.steps / t_k2        # per GPU, the dominant kernel alone
+        # per GPU, the dominant kernel alone (split mode: this rank's share of the cells)
+        k2_rate = (Bl * W if args.workload == "batched" else W / world) * args.steps / t_k2
         peak = alu_peak_cells(peak_mhz)
         line = {
             "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * t_step / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "problems": B_TOTAL, "n": N, "m": M, "semiring": "minmax",
-                       "transitions_per_problem": W, "parallelism": f"dp{world} (problems block-sharded, no collective)",
+            "config": {"workload": workload, "problems": b_total, "n": n_, "m": m_, "semiring": "minmax",
+                       "transitions_per_problem": W, "parallelism": parallelism,
                        "l2": "flushed between timed steps (256 MiB device write, untimed)"},
-            "solves_per_s": B_TOTAL * args.steps / t_step,
+            "solves_per_s": b_total * args.steps / t_step,
             "roofline": {"bound": "alu", "achieved": k2_rate / 1e9, "peak": peak / 1e9, "unit": "Gcell/s",
                          "frac": k2_rate / peak, "traffic": args.traffic,
-                         "kernel": "k2_dp_batched<F32,MINMAX>",
+                         "kernel": kernel_name,
                          "peak_basis": f"148 SMs x 4 SMSP x 32 lanes / 3 issue slots per cell x {peak_mhz:.0f} MHz "
                                        "(measured issue rates, profiles/r01_alu_peaks.jsonl)",
                          "kernel_share_of_step": t_k2 / t_step},
@@ -270,7 +289,7 @@ def run_cuda(args):
             "gpu_launches": launches,
             "clocks": clocks,
         }
-        if not args.no_cpu_baseline and world == 1:
+        if not args.no_cpu_baseline and world == 1 and args.workload == "batched":
             line["cpu_baseline"] = cpu_baseline(args.cpu_sample)
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -284,6 +303,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
+    ap.add_argument("--workload", default="batched", choices=["batched", "large"],
+                    help="batched = configs[3] (the metric's batched sweep, default); large = configs[4] split")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=2048)
     ap.add_argument("--ref-sample", type=int, default=32)

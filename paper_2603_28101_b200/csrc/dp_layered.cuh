@@ -22,6 +22,7 @@ constexpr int kK3Threads = 32 * kK3Warps;
 constexpr int kK3Cols = kK3Warps * kWarpCols;   // 512 columns per tile
 constexpr int kK3GPadLo = 23;                    // == 3 (mod 4): G staging below c0 - k1
 constexpr int kK3LPad = 24;
+constexpr int kK3MaxSlots = 1024;                // owned column blocks per rank (n <= 512K columns)
 
 struct LayerArgs {
   SolveArgs a;
@@ -33,6 +34,7 @@ struct LayerArgs {
   int nown;                  // owned-block slots per rank (ncb when own_world == 1)
   const int32_t* klo;   // [B][n+1] kv lower bounds for this layer, or null
   unsigned long long* keys;   // [B][n+1] packed (value, split) minima (KEEP_PARENTS), or null
+  unsigned long long* counter;   // [m+1] dynamic tile counters (zeroed per solve)
 };
 
 template <class D> struct AtomicBits;
@@ -253,19 +255,57 @@ __global__ void __launch_bounds__(kK3Threads) k3_layer(LayerArgs la) {
   const int cbase = j & ~3;
   const int kstart = (j - 1) & ~3;
   const int nblk = la.nown;
-  const int64_t ntiles = (int64_t)a.B * nblk * la.nq;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int q = (int)(tile % la.nq);
-    const int blk = owned_block((int)((tile / la.nq) % nblk), la.own_rank, la.own_world);
-    const int b = (int)(tile / ((int64_t)la.nq * nblk));
+  // chunk counts of this rank's blocks (identical for every problem of the batch):
+  // prefix s_pref over slots in descending block order (largest triangles first, LPT)
+  __shared__ int s_pref[kK3MaxSlots + 1];
+  __shared__ int64_t s_tile;
+  if (warp == 0) {
+    int carry = 0;
+    for (int base = 0; base < nblk; base += 32) {
+      const int sl = nblk - 1 - (base + lane);          // descending slot = descending block
+      int cnt = 0;
+      if (base + lane < nblk) {
+        const int blk = owned_block(sl, la.own_rank, la.own_world);
+        const int c0 = cbase + kK3Cols * blk;
+        if (c0 <= imax_layer) {
+          const int kend = align4(min(c0 + kK3Cols - 1, imax_layer));
+          cnt = (kend - kstart + kc - 1) / kc;
+        }
+      }
+      int incl = cnt;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += v;
+      }
+      if (base + lane < nblk) s_pref[base + lane + 1] = carry + incl;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) s_pref[0] = 0;
+  }
+  __syncthreads();
+  const int per_prob = s_pref[nblk];
+  const int64_t ntiles = (int64_t)a.B * per_prob;
+  for (;;) {
+    if (tid == 0) s_tile = (int64_t)atomicAdd(la.counter + j, 1ull);   // dynamic tile scheduler
+    __syncthreads();
+    const int64_t tile = s_tile;
+    if (tile >= ntiles) break;
+    const int b = (int)(tile / per_prob);
+    const int rr = (int)(tile % per_prob);
+    int lo = 0, hi = nblk;                  // largest idx with s_pref[idx] <= rr
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (s_pref[mid] <= rr) lo = mid; else hi = mid;
+    }
+    const int q = rr - s_pref[lo];
+    const int blk = owned_block(nblk - 1 - lo, la.own_rank, la.own_world);
     const int c0 = cbase + kK3Cols * blk;
-    if (c0 > imax_layer) continue;                              // (uniform across the CTA)
     const int imaxb = min(c0 + kK3Cols - 1, imax_layer);
     const int kend = align4(imaxb);
     const int k0 = kstart + q * kc;
-    if (k0 >= kend) continue;
     const int k1 = min(k0 + kc, kend);
-    if (a.status[b] != HEDDLE_OK) continue;
+    if (a.status[b] != HEDDLE_OK) { __syncthreads(); continue; }
     const L* gL = reinterpret_cast<const L*>(a.lengths) + (int64_t)b * a.ls;
     const D* gprev = reinterpret_cast<const D*>(a.dpws) + ((int64_t)b * (m + 1) + (j - 1)) * (n + 1);
     D* gcur = reinterpret_cast<D*>(a.dpws) + ((int64_t)b * (m + 1) + j) * (n + 1);
@@ -276,7 +316,6 @@ __global__ void __launch_bounds__(kK3Threads) k3_layer(LayerArgs la) {
     const int cap = a.caps ? a.caps[(int64_t)b * a.cs + j - 1] : -1;
     const int ghi = (cap >= 0 && cap < n) ? cap : n;
     // ---- stage: splits [k0, k1) (+inf / 1 beyond k1 so quarter overruns contribute nothing)
-    __syncthreads();   // previous tile's readers are done
     for (int t = tid; t < kc + kK3LPad; t += kK3Threads) {
       const int k = k0 + t;
       const bool in = k < k1;
@@ -342,6 +381,7 @@ __global__ void __launch_bounds__(kK3Threads) k3_layer(LayerArgs la) {
         }
       }
     }
+    __syncthreads();   // staged rows and s_tile are reused by the next tile
   }
 }
 

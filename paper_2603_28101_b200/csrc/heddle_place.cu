@@ -9,6 +9,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <cstdio>
 #include <new>
 #include <vector>
 
@@ -64,6 +65,7 @@ struct heddle_place_ctx {
   int num_sms = 0;
   int32_t* d_klo = nullptr;             // [max_batch][max_n+1] (layered kernel, kv caps)
   unsigned long long* d_keys = nullptr; // [max_batch][max_n+1] (layered kernel, KEEP_PARENTS)
+  unsigned long long* d_ctr = nullptr;  // [max_m+1] dynamic tile counters of the layered kernel
   bool last_layered = false;
   // split mode (one large instance over several GPUs)
   int split_rank = 0, split_world = 1;
@@ -72,6 +74,8 @@ struct heddle_place_ctx {
   void* d_send = nullptr;
   void* d_recv = nullptr;
   size_t xbuf_bytes = 0;
+  // tracing (HEDDLE_PLACE_TRACE=1): per-phase device time of the layered path, printed per solve
+  bool trace = false;
 };
 
 namespace {
@@ -226,13 +230,18 @@ heddle_status solve_layered(heddle_place_ctx* x, SolveArgs& a, bool kp, bool kv,
     if (cudaMalloc(&x->d_keys, 8 * (size_t)x->max_batch * (x->max_n + 1)) != cudaSuccess) { cudaGetLastError(); return HEDDLE_E_NOMEM; }
     if (cudaMemsetAsync(x->d_keys, 0xff, 8 * (size_t)x->max_batch * (x->max_n + 1), s) != cudaSuccess) return HEDDLE_E_CUDA;
   }
+  if (!x->d_ctr) {
+    if (cudaMalloc(&x->d_ctr, 8 * (size_t)(x->max_m + 1)) != cudaSuccess) { cudaGetLastError(); return HEDDLE_E_NOMEM; }
+  }
+  if (cudaMemsetAsync(x->d_ctr, 0, 8 * (size_t)(m + 1), s) != cudaSuccess) return HEDDLE_E_CUDA;
   const int64_t cells = (int64_t)B * (m + 1) * (n + 1);
   const int fill_grid = (int)std::min<int64_t>((cells + 255) / 256, (int64_t)x->num_sms * 16);
   HP_DISPATCH(fill_launch, a, cells, fill_grid, s);
   pro_for(dt, sr, kp, kv)<<<B, 256, 0, s>>>(a);
   x->launches += 2;
   // tile geometry: 256 columns x kc splits; kc sized for >= ~4 tiles per resident CTA
-  const double layer_cells = (double)B * (double)(n - m + 1) * (double)(n - m + 2) / 2.0;
+  // (per rank in split mode: each rank computes 1/world of the layer's cells)
+  const double layer_cells = (double)B * (double)(n - m + 1) * (double)(n - m + 2) / 2.0 / x->split_world;
   K3Fn fn = k3_for(dt, sr, kp, kv);
   int kc = 2048;
   int occ = 0;
@@ -257,6 +266,8 @@ heddle_status solve_layered(heddle_place_ctx* x, SolveArgs& a, bool kp, bool kv,
   la.nown = owned_slots(la.ncb, world);
   la.klo = kv ? x->d_klo : nullptr;
   la.keys = kp ? x->d_keys : nullptr;
+  la.counter = x->d_ctr;
+  if (la.nown > kK3MaxSlots) return HEDDLE_E_INVALID;
   const int64_t ntiles = (int64_t)B * la.nown * la.nq;
   const int grid = (int)std::min<int64_t>(ntiles, (int64_t)occ * x->num_sms);
   // split-mode exchange buffers: send [B][nown][kK3Cols], recv [world][B][nown][kK3Cols]
@@ -277,6 +288,11 @@ heddle_status solve_layered(heddle_place_ctx* x, SolveArgs& a, bool kp, bool kv,
                             : (sr == HEDDLE_MINMAX ? ncclUint32 : ncclUint64);
   const dim3 pg((unsigned)std::min<int64_t>((slab / B + 255) / 256, 1024), B);
   const dim3 ug((unsigned)std::min<int64_t>((slab * world / B + 255) / 256, 2048), B);
+  std::vector<cudaEvent_t> tev;
+  if (x->trace) {
+    tev.resize(3 * (size_t)m);
+    for (auto& e : tev) cudaEventCreate(&e);
+  }
   for (int j = 2; j <= m; ++j) {
     la.j = j;
     if (kv) {
@@ -284,11 +300,13 @@ heddle_status solve_layered(heddle_place_ctx* x, SolveArgs& a, bool kp, bool kv,
       HP_DISPATCH(klo_launch, a, j, x->d_klo, g, s);
       x->launches++;
     }
+    if (x->trace) cudaEventRecord(tev[3 * j - 6], s);
     if (world > 1 && x->split_emulate) {
       // every virtual rank computes its blocks; the all-gather is emulated by packing each
       // rank's blocks into its recv slab, clearing the row and unpacking it again
       for (int vr = 0; vr < world; ++vr) {
         la.own_rank = vr;
+        if (cudaMemsetAsync(x->d_ctr + j, 0, 8, s) != cudaSuccess) return HEDDLE_E_CUDA;
         fn<<<grid, kK3Threads, smem, s>>>(la);
         x->launches++;
       }
@@ -302,6 +320,7 @@ heddle_status solve_layered(heddle_place_ctx* x, SolveArgs& a, bool kp, bool kv,
     } else {
       fn<<<grid, kK3Threads, smem, s>>>(la);
       x->launches++;
+      if (x->trace) cudaEventRecord(tev[3 * j - 5], s);
       if (world > 1) {
         HP_DISPATCH(pack_launch, a, j, x->split_rank, world, la.nown, x->d_send, pg, s);
         if (ncclAllGather(x->d_send, x->d_recv, slab, nt, x->comm, s) != ncclSuccess) return HEDDLE_E_NCCL;
@@ -309,11 +328,26 @@ heddle_status solve_layered(heddle_place_ctx* x, SolveArgs& a, bool kp, bool kv,
         x->launches += 2;
       }
     }
+    if (x->trace) cudaEventRecord(tev[3 * j - 4], s);
     if (kp) {
       dim3 g((n + 256) / 256, B);
       HP_DISPATCH(unpack_launch, a, j, x->d_keys, g, s);
       x->launches++;
     }
+  }
+  if (x->trace) {
+    cudaStreamSynchronize(s);
+    float tk = 0, tx = 0, ms = 0, mx = 0;
+    for (int j = 2; j <= m; ++j) {
+      cudaEventElapsedTime(&ms, tev[3 * j - 6], tev[3 * j - 5]);
+      tk += ms;
+      cudaEventElapsedTime(&ms, tev[3 * j - 5], tev[3 * j - 4]);
+      tx += ms;
+      mx = ms > mx ? ms : mx;
+    }
+    std::fprintf(stderr, "[heddle_place trace] rank %d/%d n=%d m=%d B=%d kc=%d grid=%d: layer kernels %.3f ms, "
+                 "exchange %.3f ms (max %.1f us/layer)\n", x->split_rank, world, n, m, B, kc, grid, tk, tx, 1e3 * mx);
+    for (auto& e : tev) cudaEventDestroy(e);
   }
   HP_DISPATCH(finalize_launch, a, s);
   x->launches++;
@@ -361,6 +395,7 @@ void heddle_place_destroy(heddle_place_ctx* ctx) {
   cudaFree(ctx->d_stage);
   cudaFree(ctx->d_klo);
   cudaFree(ctx->d_keys);
+  cudaFree(ctx->d_ctr);
   cudaFree(ctx->d_send);
   cudaFree(ctx->d_recv);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
@@ -418,6 +453,10 @@ heddle_status heddle_place_init(const heddle_place_config* c, heddle_place_ctx**
   x->flags = c->flags;
   x->gstride = c->max_n + 1;
   x->lmax_u32 = lmax;
+  {
+    const char* tr = std::getenv("HEDDLE_PLACE_TRACE");
+    x->trace = tr && tr[0] == '1';
+  }
   cudaDeviceGetAttribute(&x->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device);
   cudaDeviceGetAttribute(&x->num_sms, cudaDevAttrMultiProcessorCount, c->device);
 
