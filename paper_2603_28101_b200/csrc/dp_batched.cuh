@@ -372,8 +372,10 @@ __global__ void __launch_bounds__(kK2Threads) k2_dp_batched(SolveArgs a) {
         if (KP) gpar[(int64_t)m * (n + 1) + n] = (v == T::inf()) ? -1 : bk;
       }
     } else {
-      const int cbase = j & ~3;
-      const int nblk = (imax_layer - cbase) / kWarpCols + 1;
+      // column blocks anchored at the TOP of the computed region (<= 3 surplus columns there);
+      // the surplus of the partial block falls below column j, where split ranges are short
+      const int ctop = align4(imax_layer - (kWarpCols - 1));
+      const int nblk = (ctop + kWarpCols - 1 - j) / kWarpCols + 1;
       const int kstart = (j - 1) & ~3;
       const int cl = lane & (kColLanes - 1), kg = lane / kColLanes;
       for (;;) {
@@ -381,7 +383,7 @@ __global__ void __launch_bounds__(kK2Threads) k2_dp_batched(SolveArgs a) {
         if (lane == 0) t = atomicAdd(&s_ctr, 1);
         t = __shfl_sync(0xffffffffu, t, 0);
         if (t >= nblk) break;
-        const int cb = cbase + kWarpCols * (nblk - 1 - t);   // longest block first (LPT)
+        const int cb = ctop - kWarpCols * t;                  // longest block first (LPT)
         const int c = cb + kLaneCols * cl;
         const int imax = min(cb + kWarpCols - 1, imax_layer);
         const int kend = align4(imax);                       // splits k <= imax - 1
