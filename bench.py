@@ -46,6 +46,21 @@ def peaks():
         return {}
 
 
+def ncu_traffic(workload):
+    """DRAM bytes (read + write) per launch of the dominant kernel from the committed ncu summary
+    (profiles/*_k2_ncu_summary.json, one `ncu --set full` capture), or None."""
+    import glob
+    if workload != "batched":
+        return None
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_k2_ncu_summary.json")))
+    if not files:
+        return None
+    try:
+        return json.load(open(files[-1])).get("traffic_bytes")
+    except Exception:
+        return None
+
+
 def alu_peak_cells(sm_mhz):
     """Issue-bound peak of the exhaustive Eq. 3 reduction: 4 SMSPs x 1 warp-instr/clk x 32 lanes
     / 3 instructions per transition, x 148 SMs x clock."""
@@ -279,7 +294,9 @@ def run_cuda(args):
                        "l2": "flushed between timed steps (256 MiB device write, untimed)"},
             "solves_per_s": b_total * args.steps / t_step,
             "roofline": {"bound": "alu", "achieved": k2_rate / 1e9, "peak": peak / 1e9, "unit": "Gcell/s",
-                         "frac": k2_rate / peak, "traffic": args.traffic,
+                         "frac": k2_rate / peak,
+                         "traffic": args.traffic if args.traffic is not None else ncu_traffic(args.workload),
+                         "algorithmic_bytes": (4 * n_ + 4 * m_ + 4 + 4 * (m_ + 1)) * (Bl if args.workload == "batched" else 1),
                          "kernel": kernel_name,
                          "peak_basis": f"148 SMs x 4 SMSP x 32 lanes / 3 issue slots per cell x {peak_mhz:.0f} MHz "
                                        "(measured issue rates, profiles/r01_alu_peaks.jsonl)",

@@ -31,8 +31,11 @@
 namespace hp {
 
 constexpr int kLaneCols = 8;                 // columns per lane (R)
-constexpr int kColLanes = 8;                 // lanes across columns
-constexpr int kSplitLanes = 4;               // lanes across splits k, each owning a contiguous quarter
+#ifndef HEDDLE_COL_LANES
+#define HEDDLE_COL_LANES 8
+#endif
+constexpr int kColLanes = HEDDLE_COL_LANES;  // lanes across columns
+constexpr int kSplitLanes = 32 / kColLanes;  // lanes across splits k, each owning a contiguous part
 constexpr int kWarpCols = kColLanes * kLaneCols;   // 64 columns per warp task
 constexpr int kGPad = 131;                   // G padding below s = 0; == 3 (mod 4) for LDS.128 alignment
 constexpr int kGTail = kWarpCols + 8;        // G padding above s = n
