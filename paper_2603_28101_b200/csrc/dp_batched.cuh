@@ -67,6 +67,7 @@ struct SolveArgs {
   int32_t* status;         // [B] workspace status
   int32_t* status_out;     // [B] caller's status or null
   void* objective;         // [B] caller's objective
+  int* err;                // split mode: set by a peer-exchange timeout (reported as E_NCCL), or null
 };
 
 __host__ __device__ inline int align4(int x) { return (x + 3) & ~3; }

@@ -35,7 +35,46 @@ struct LayerArgs {
   const int32_t* klo;   // [B][n+1] kv lower bounds for this layer, or null
   unsigned long long* keys;   // [B][n+1] packed (value, split) minima (KEEP_PARENTS), or null
   unsigned long long* counter;   // [m+1] dynamic tile counters (zeroed per solve)
+  // ---- fused NVLink exchange (split mode over peer memory) ----
+  void* const* peer_dp;          // [world] every rank's dp workspace (peer pointers via CUDA IPC), or null
+  unsigned long long* const* peer_flags;   // [world] every rank's arrival counters [m+1]
+  unsigned long long* flags;     // this rank's arrival counters (peers add 1 per pushed block)
+  unsigned int* blk_done;        // [B][ncb] finished tiles per column block of this layer (zeroed per layer)
+  unsigned long long wait_prev;  // flags[j-1] target before reading row j-1 (0: no wait)
+  unsigned long long wait_start; // flags[0] target before pushing into peers (solve-start barrier)
+  int* err;                      // set on a spin timeout (never hang the device)
 };
+
+// L2 load (bypasses L1: values were produced by other CTAs' atomics)
+template <class D>
+__device__ __forceinline__ D ld_cg(const D* p) {
+  if constexpr (sizeof(D) == 4) {
+    const unsigned v = __ldcg(reinterpret_cast<const unsigned*>(p));
+    return *reinterpret_cast<const D*>(&v);
+  } else {
+    const unsigned long long v = __ldcg(reinterpret_cast<const unsigned long long*>(p));
+    return *reinterpret_cast<const D*>(&v);
+  }
+}
+
+// Spin until *flag >= target (acquire), with a ~10 s timeout that raises *err.
+__device__ __forceinline__ bool wait_flag(const unsigned long long* flag, unsigned long long target, int* err) {
+  if (target == 0) return true;
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+    if (v >= target) return true;
+    unsigned long long t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    if (t1 - t0 > 10000000000ull || *(volatile int*)err) {
+      atomicExch(err, 1);
+      return false;
+    }
+    __nanosleep(200);
+  }
+}
 
 template <class D> struct AtomicBits;
 template <> struct AtomicBits<float> {
@@ -286,6 +325,12 @@ __global__ void __launch_bounds__(kK3Threads) k3_layer(LayerArgs la) {
   __syncthreads();
   const int per_prob = s_pref[nblk];
   const int64_t ntiles = (int64_t)a.B * per_prob;
+  if (la.peer_dp) {   // fused exchange: row j-1 must have arrived from every peer
+    __shared__ int s_ok;
+    if (tid == 0) s_ok = wait_flag(la.flags + (j - 1), la.wait_prev, la.err);
+    __syncthreads();
+    if (!s_ok) return;
+  }
   for (;;) {
     if (tid == 0) s_tile = (int64_t)atomicAdd(la.counter + j, 1ull);   // dynamic tile scheduler
     __syncthreads();
@@ -381,8 +426,50 @@ __global__ void __launch_bounds__(kK3Threads) k3_layer(LayerArgs la) {
         }
       }
     }
+    if (la.peer_dp) {
+      // last finished tile of a column block pushes the block's final row values to every peer
+      // over NVLink (vector stores into the peers' dp rows), then bumps their arrival counter
+      __shared__ int s_last;
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) {
+        const int nch = (kend - kstart + kc - 1) / kc;
+        s_last = atomicAdd(la.blk_done + (int64_t)b * la.ncb + blk, 1u) == (unsigned)(nch - 1);
+        if (s_last) s_last = wait_flag(la.flags, la.wait_start, la.err);
+      }
+      __syncthreads();
+      if (s_last) {
+        __threadfence();
+        const int64_t roff = ((int64_t)b * (m + 1) + j) * (n + 1);
+        const D* mine = reinterpret_cast<const D*>(a.dpws) + roff;
+        const int lo = max(c0, j), hi = imaxb;   // valid columns of this block
+        for (int r = 0; r < la.own_world; ++r) {
+          if (r == la.own_rank) continue;
+          D* dst = reinterpret_cast<D*>(la.peer_dp[r]) + roff;
+          for (int i = lo + tid; i <= hi; i += kK3Threads) dst[i] = ld_cg(mine + i);
+        }
+        __threadfence_system();
+        __syncthreads();
+        if (tid == 0)
+          for (int r = 0; r < la.own_world; ++r)
+            if (r != la.own_rank) atomicAdd_system(la.peer_flags[r] + j, 1ull);
+      }
+    }
     __syncthreads();   // staged rows and s_tile are reused by the next tile
   }
+}
+
+// ---------------------------------------------------------------- fused exchange helpers
+// solve-start barrier: announce to every peer that this rank's workspace is reset
+__global__ void k3_signal_start(unsigned long long* const* peer_flags, int rank, int world) {
+  __threadfence_system();
+  for (int r = 0; r < world; ++r)
+    if (r != rank) atomicAdd_system(peer_flags[r], 1ull);
+}
+// wait for the last layer's blocks from every peer before finalising / backtracking
+__global__ void k3_wait(const unsigned long long* flag, unsigned long long target, int* err) {
+  wait_flag(flag, target, err);
+  __threadfence();
 }
 
 // ---------------------------------------------------------------- KEEP_PARENTS: unpack keys of layer j
@@ -413,7 +500,9 @@ __global__ void k3_finalize(SolveArgs a) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= a.B) return;
   const int n = a.n, m = a.m;
+  if (a.err && *(volatile int*)a.err) a.status[b] = HEDDLE_E_NCCL;   // peer exchange timed out
   if (a.status[b] != HEDDLE_OK) {
+    if (a.status_out) a.status_out[b] = a.status[b];
     if constexpr (DT == HEDDLE_U32 && SR == HEDDLE_MINPLUS) reinterpret_cast<uint64_t*>(a.objective)[b] = ~0ull;
     else reinterpret_cast<D*>(a.objective)[b] = T::inf();
     return;

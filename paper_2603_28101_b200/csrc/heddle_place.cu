@@ -76,6 +76,16 @@ struct heddle_place_ctx {
   size_t xbuf_bytes = 0;
   // tracing (HEDDLE_PLACE_TRACE=1): per-phase device time of the layered path, printed per solve
   bool trace = false;
+  // fused NVLink exchange (split mode): peers' dp workspaces and arrival counters via CUDA IPC
+  bool p2p = false;
+  void** d_peer_dp = nullptr;                 // device array [world]
+  unsigned long long** d_peer_flags = nullptr; // device array [world]
+  unsigned long long* d_flags = nullptr;      // [max_m+1] this rank's arrival counters (monotonic)
+  std::vector<void*> peer_dp_h, peer_flags_h; // opened IPC mappings (host copies, for cleanup)
+  unsigned int* d_blkdone = nullptr;          // [max_batch][ncb_max]
+  int* d_err = nullptr;
+  int64_t epoch = 0;                          // collective solves so far (same on every rank)
+  std::vector<unsigned long long> expect;     // cumulative arrivals expected per counter
 };
 
 namespace {
@@ -293,12 +303,44 @@ heddle_status solve_layered(heddle_place_ctx* x, SolveArgs& a, bool kp, bool kv,
     tev.resize(3 * (size_t)m);
     for (auto& e : tev) cudaEventCreate(&e);
   }
+  const bool p2p = world > 1 && x->p2p && !x->split_emulate;
+  if (p2p) {
+    // fused NVLink exchange: counters are monotonic across solves; expected arrivals are
+    // accumulated per layer (blocks with computed columns owned by the other ranks)
+    x->epoch++;
+    if ((int)x->expect.size() < x->max_m + 1) x->expect.assign(x->max_m + 1, 0ull);
+    x->expect[0] += (unsigned long long)(world - 1);
+    if (cudaMemsetAsync(x->d_blkdone, 0, sizeof(unsigned) * (size_t)B * la.ncb * (m + 1), s) != cudaSuccess)
+      return HEDDLE_E_CUDA;
+    k3_signal_start<<<1, 1, 0, s>>>(x->d_peer_flags, x->split_rank, world);
+    x->launches++;
+    la.peer_dp = x->d_peer_dp;
+    la.peer_flags = x->d_peer_flags;
+    la.flags = x->d_flags;
+    la.err = x->d_err;
+    la.a.err = x->d_err;
+    la.wait_start = x->expect[0];
+  }
   for (int j = 2; j <= m; ++j) {
     la.j = j;
     if (kv) {
       dim3 g((n + 256) / 256, B);
       HP_DISPATCH(klo_launch, a, j, x->d_klo, g, s);
       x->launches++;
+    }
+    if (p2p) {
+      la.blk_done = x->d_blkdone + (size_t)B * la.ncb * j;
+      la.wait_prev = j >= 3 ? x->expect[j - 1] : 0ull;
+      // arrivals for row j: one per (problem, block with computed columns) owned by another rank
+      const int cbase = j & ~3, imax = n - m + j;
+      int foreign = 0;
+      for (int blk = 0; blk < la.ncb; ++blk) {
+        if (cbase + kK3Cols * blk > imax) break;
+        const int w = blk % (2 * world);
+        const int owner = w < world ? w : 2 * world - 1 - w;   // inverse of owned_block()
+        if (owner != x->split_rank) ++foreign;
+      }
+      x->expect[j] += (unsigned long long)foreign * B;
     }
     if (x->trace) cudaEventRecord(tev[3 * j - 6], s);
     if (world > 1 && x->split_emulate) {
@@ -321,7 +363,7 @@ heddle_status solve_layered(heddle_place_ctx* x, SolveArgs& a, bool kp, bool kv,
       fn<<<grid, kK3Threads, smem, s>>>(la);
       x->launches++;
       if (x->trace) cudaEventRecord(tev[3 * j - 5], s);
-      if (world > 1) {
+      if (world > 1 && !p2p) {
         HP_DISPATCH(pack_launch, a, j, x->split_rank, world, la.nown, x->d_send, pg, s);
         if (ncclAllGather(x->d_send, x->d_recv, slab, nt, x->comm, s) != ncclSuccess) return HEDDLE_E_NCCL;
         HP_DISPATCH(unpack_rows_launch, a, j, world, la.nown, x->d_recv, ug, s);
@@ -334,6 +376,10 @@ heddle_status solve_layered(heddle_place_ctx* x, SolveArgs& a, bool kp, bool kv,
       HP_DISPATCH(unpack_launch, a, j, x->d_keys, g, s);
       x->launches++;
     }
+  }
+  if (p2p) {   // the last row must have arrived before the finaliser and the backtrack read it
+    k3_wait<<<1, 1, 0, s>>>(x->d_flags + m, m >= 2 ? x->expect[m] : 0ull, x->d_err);
+    x->launches++;
   }
   if (x->trace) {
     cudaStreamSynchronize(s);
@@ -349,6 +395,7 @@ heddle_status solve_layered(heddle_place_ctx* x, SolveArgs& a, bool kp, bool kv,
                  "exchange %.3f ms (max %.1f us/layer)\n", x->split_rank, world, n, m, B, kc, grid, tk, tx, 1e3 * mx);
     for (auto& e : tev) cudaEventDestroy(e);
   }
+  if (p2p) a.err = x->d_err;
   HP_DISPATCH(finalize_launch, a, s);
   x->launches++;
   return cudaGetLastError() == cudaSuccess ? HEDDLE_OK : HEDDLE_E_CUDA;
@@ -398,6 +445,15 @@ void heddle_place_destroy(heddle_place_ctx* ctx) {
   cudaFree(ctx->d_ctr);
   cudaFree(ctx->d_send);
   cudaFree(ctx->d_recv);
+  for (size_t r = 0; r < ctx->peer_dp_h.size(); ++r)
+    if ((int)r != ctx->split_rank && ctx->peer_dp_h[r]) cudaIpcCloseMemHandle(ctx->peer_dp_h[r]);
+  for (size_t r = 0; r < ctx->peer_flags_h.size(); ++r)
+    if ((int)r != ctx->split_rank && ctx->peer_flags_h[r]) cudaIpcCloseMemHandle(ctx->peer_flags_h[r]);
+  cudaFree(ctx->d_peer_dp);
+  cudaFree(ctx->d_peer_flags);
+  cudaFree(ctx->d_flags);
+  cudaFree(ctx->d_blkdone);
+  cudaFree(ctx->d_err);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   delete ctx;
 }
@@ -670,6 +726,78 @@ heddle_status heddle_place_nccl_unique_id(void* id_out, int32_t bytes) {
   return HEDDLE_OK;
 }
 
+// Exchange CUDA IPC handles of the dp workspace and the arrival counters over NCCL and map
+// every peer's buffers (NVLink peer memory).  Returns OK without enabling P2P when the
+// devices cannot access each other (the NCCL all-gather exchange is used then).
+static heddle_status setup_p2p(heddle_place_ctx* x) {
+  const int world = x->split_world, rank = x->split_rank;
+  DeviceGuard guard(x->device);
+  const int ncb_max = (x->max_n + 3) / kK3Cols + 2;
+  if (cudaMalloc(&x->d_flags, 8 * (size_t)(x->max_m + 1)) != cudaSuccess ||
+      cudaMemset(x->d_flags, 0, 8 * (size_t)(x->max_m + 1)) != cudaSuccess ||
+      cudaMalloc(&x->d_blkdone, sizeof(unsigned) * (size_t)x->max_batch * ncb_max * (x->max_m + 1)) != cudaSuccess ||
+      cudaMalloc(&x->d_err, sizeof(int)) != cudaSuccess || cudaMemset(x->d_err, 0, sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&x->d_peer_dp, sizeof(void*) * world) != cudaSuccess ||
+      cudaMalloc(&x->d_peer_flags, sizeof(void*) * world) != cudaSuccess) {
+    cudaGetLastError();
+    return HEDDLE_E_NOMEM;
+  }
+  cudaIpcMemHandle_t mine[2];
+  if (cudaIpcGetMemHandle(&mine[0], x->d_dp) != cudaSuccess || cudaIpcGetMemHandle(&mine[1], x->d_flags) != cudaSuccess) {
+    cudaGetLastError();
+    return HEDDLE_OK;   // no IPC: keep the NCCL exchange
+  }
+  char *dsend = nullptr, *drecv = nullptr;
+  const size_t hb = sizeof(mine);
+  if (cudaMalloc(&dsend, hb) != cudaSuccess || cudaMalloc(&drecv, hb * world) != cudaSuccess) return HEDDLE_E_NOMEM;
+  cudaMemcpy(dsend, mine, hb, cudaMemcpyHostToDevice);
+  ncclResult_t nr = ncclAllGather(dsend, drecv, hb, ncclChar, x->comm, 0);
+  std::vector<cudaIpcMemHandle_t> all(2 * world);
+  if (nr == ncclSuccess) cudaMemcpy(all.data(), drecv, hb * world, cudaMemcpyDeviceToHost);
+  cudaFree(dsend);
+  cudaFree(drecv);
+  if (nr != ncclSuccess) return HEDDLE_E_NCCL;
+  // every rank must be able to reach every peer; decide collectively (min over ranks)
+  int ok = 1;
+  int ndev = 0;
+  cudaGetDeviceCount(&ndev);
+  x->peer_dp_h.assign(world, nullptr);
+  x->peer_flags_h.assign(world, nullptr);
+  for (int r = 0; r < world && ok; ++r) {
+    if (r == rank) {
+      x->peer_dp_h[r] = x->d_dp;
+      x->peer_flags_h[r] = x->d_flags;
+      continue;
+    }
+    if (cudaIpcOpenMemHandle(&x->peer_dp_h[r], all[2 * r], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
+        cudaIpcOpenMemHandle(&x->peer_flags_h[r], all[2 * r + 1], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      ok = 0;
+    }
+  }
+  int* dok = nullptr;
+  cudaMalloc(&dok, sizeof(int));
+  cudaMemcpy(dok, &ok, sizeof(int), cudaMemcpyHostToDevice);
+  nr = ncclAllReduce(dok, dok, 1, ncclInt32, ncclMin, x->comm, 0);
+  cudaMemcpy(&ok, dok, sizeof(int), cudaMemcpyDeviceToHost);
+  cudaFree(dok);
+  if (nr != ncclSuccess) return HEDDLE_E_NCCL;
+  if (!ok) {
+    for (int r = 0; r < world; ++r) {
+      if (r == rank) continue;
+      if (x->peer_dp_h[r]) cudaIpcCloseMemHandle(x->peer_dp_h[r]);
+      if (x->peer_flags_h[r]) cudaIpcCloseMemHandle(x->peer_flags_h[r]);
+    }
+    x->peer_dp_h.clear();
+    x->peer_flags_h.clear();
+    return HEDDLE_OK;
+  }
+  cudaMemcpy(x->d_peer_dp, x->peer_dp_h.data(), sizeof(void*) * world, cudaMemcpyHostToDevice);
+  cudaMemcpy(x->d_peer_flags, x->peer_flags_h.data(), sizeof(void*) * world, cudaMemcpyHostToDevice);
+  x->p2p = cudaGetLastError() == cudaSuccess;
+  return HEDDLE_OK;
+}
+
 heddle_status heddle_place_init_split(const heddle_place_config* cfg, const void* nccl_unique_id, int32_t rank,
                                       int32_t world, heddle_place_ctx** out) {
   if (!out) return HEDDLE_E_INVALID;
@@ -695,6 +823,14 @@ heddle_status heddle_place_init_split(const heddle_place_config* cfg, const void
         x->comm = nullptr;
         heddle_place_destroy(x);
         return HEDDLE_E_NCCL;
+      }
+      const char* ex = std::getenv("HEDDLE_PLACE_EXCHANGE");   // "nccl" forces the all-gather exchange
+      if (!(ex && std::strcmp(ex, "nccl") == 0)) {
+        st = setup_p2p(x);
+        if (st != HEDDLE_OK) {
+          heddle_place_destroy(x);
+          return st;
+        }
       }
     }
   }
