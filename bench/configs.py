@@ -55,20 +55,23 @@ def main():
             pl.solve(L, D)
             pl.backtrack()
         torch.cuda.synchronize()
-        times = []
+        times, tsolve = [], []
         l0 = pl.launches
         for _ in range(args.reps):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
             e0.record()
             pl.solve(L, D)
+            e2.record()
             pl.backtrack()
             e1.record()
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1) / 1e3)
+            tsolve.append(e0.elapsed_time(e2) / 1e3)
         t = float(np.median(times))
+        ts = float(np.median(tsolve))
         W = b.B * _lib.transitions(b.n, b.m)
         print(json.dumps({"config": name, "n": b.n, "m": b.m, "B": b.B, "dtype": b.profile.dtype,
-                          "ms": 1e3 * t, "cells": W, "cells_per_s": W / t, "solves_per_s": b.B / t,
+                          "ms": 1e3 * t, "ms_solve": 1e3 * ts, "ms_backtrack": 1e3 * (t - ts), "cells": W, "cells_per_s": W / t, "solves_per_s": b.B / t,
                           "frac_alu_roofline": W / t / peak,
                           "launches_per_solve": (pl.launches - l0) / args.reps}), flush=True)
         pl.close()

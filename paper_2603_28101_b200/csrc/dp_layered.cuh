@@ -306,7 +306,8 @@ __global__ void __launch_bounds__(kK3Threads) k3_layer(LayerArgs la) {
       if (base + lane < nblk) {
         const int blk = owned_block(sl, la.own_rank, la.own_world);
         const int c0 = cbase + kK3Cols * blk;
-        if (c0 <= imax_layer) {
+        // (last layer: only the state i = n is on a complete partition -- R8)
+        if (c0 <= imax_layer && (j < m || c0 + kK3Cols > n)) {
           const int kend = align4(min(c0 + kK3Cols - 1, imax_layer));
           cnt = (kend - kstart + kc - 1) / kc;
         }
@@ -457,6 +458,171 @@ __global__ void __launch_bounds__(kK3Threads) k3_layer(LayerArgs la) {
     }
     __syncthreads();   // staged rows and s_tile are reused by the next tile
   }
+}
+
+// ================================================================ K5: persistent dataflow DP
+// One persistent launch computes every layer j = 2..m.  Tiles (layer, column block,
+// split chunk) are dequeued in layer order from a global counter; a tile first waits
+// until the blocks of row j-1 covering its split range are final (per-block "ready"
+// counters, monotonic per solve), so layer j+1 starts on its low splits while layer j
+// is still finishing its high columns: no per-layer launch, barrier or tail.  The
+// tile that completes a column block publishes it: it bumps the block's ready counter
+// and, in split mode, first stores the block's final values into every peer's dp row
+// over NVLink (CUDA-IPC peer memory) and bumps the peers' counters (system scope).
+// Deadlock freedom: every dependency of a tile was dequeued earlier, by a running CTA.
+struct PersistArgs {
+  SolveArgs a;
+  int kc, ncb;
+  const int4* tiles;               // [nentries] {j, blk, q, nch(blk)}; problems interleaved b-minor
+  int64_t nentries;
+  unsigned long long* counter;     // global tile counter (zeroed per solve)
+  unsigned int* blk_done;          // [m+1][B][ncb] finished tiles per block (zeroed per solve)
+  unsigned long long* ready;       // [m+1][B][ncb] epoch counters of this rank
+  unsigned long long epoch;        // solves so far including this one (same on every rank)
+  int own_rank, own_world;
+  void* const* peer_dp;            // split mode: every rank's dp workspace (null: single GPU)
+  unsigned long long* const* peer_ready;   // split mode: every rank's ready array
+  const unsigned long long* start_flag;    // split mode: solve-start barrier counter
+  unsigned long long wait_start;
+  int* err;
+};
+
+template <int DT, int SR>
+__global__ void __launch_bounds__(kK3Threads) k5_persistent(PersistArgs pa) {
+  using T = Tr<DT, SR>;
+  using L = typename T::L;
+  using G = typename T::G;
+  using D = typename T::D;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const SolveArgs& a = pa.a;
+  const int n = a.n, m = a.m, B = a.B, kc = pa.kc, ncb = pa.ncb;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int cl = lane & (kColLanes - 1), kg = lane / kColLanes;
+  const K3Smem<DT, SR> lay(kc);
+  L* sL = reinterpret_cast<L*>(smem + lay.lOff);
+  D* sdp = reinterpret_cast<D*>(smem + lay.dOff);
+  G* sG = reinterpret_cast<G*>(smem + lay.gOff);
+  G* sG2 = reinterpret_cast<G*>(smem + lay.g2Off);
+  __shared__ int64_t s_tile;
+  __shared__ int s_flag;
+  const int64_t ntiles = pa.nentries * B;
+  for (;;) {
+    if (tid == 0) s_tile = (int64_t)atomicAdd(pa.counter, 1ull);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    if (tile >= ntiles) break;
+    const int4 tl = pa.tiles[tile / B];
+    const int b = (int)(tile % B);
+    const int j = tl.x, blk = tl.y, q = tl.z, nch = tl.w;
+    const int imax_layer = n - m + j;
+    const int cbase = j & ~3, kstart = (j - 1) & ~3;
+    const int c0 = cbase + kK3Cols * blk;
+    const int imaxb = min(c0 + kK3Cols - 1, imax_layer);
+    const int kend = align4(imaxb);
+    const int k0 = kstart + q * kc;
+    const int k1 = min(k0 + kc, kend);
+    if (a.status[b] != HEDDLE_OK) { __syncthreads(); continue; }   // (uniform; consumers skip it too)
+    // ---- dependencies: row j-1 columns [max(k0, j-1), min(k1-1, n-m+j-1)] final (row 1: prologue)
+    if (j >= 3) {
+      if (tid == 0) {
+        const int pc = (j - 1) & ~3;
+        const int lo = max(k0, j - 1), hi = min(k1 - 1, n - m + j - 1);
+        int ok = 1;
+        for (int bb = (lo - pc) / kK3Cols; ok && bb <= (hi - pc) / kK3Cols; ++bb)
+          ok = wait_flag(pa.ready + ((int64_t)(j - 1) * B + b) * ncb + bb, pa.epoch, pa.err);
+        s_flag = ok;
+      }
+      __syncthreads();
+      if (!s_flag) break;
+    }
+    const L* gL = reinterpret_cast<const L*>(a.lengths) + (int64_t)b * a.ls;
+    const D* gprev = reinterpret_cast<const D*>(a.dpws) + ((int64_t)b * (m + 1) + (j - 1)) * (n + 1);
+    D* gcur = reinterpret_cast<D*>(a.dpws) + ((int64_t)b * (m + 1) + j) * (n + 1);
+    int row = 0;
+    const int d = a.degrees[(int64_t)b * a.ds + j - 1];
+    for (int qq = 0; qq < a.D; ++qq) row = (a.prof_deg[qq] == d) ? qq : row;
+    const G* grow = reinterpret_cast<const G*>(a.gtab) + (int64_t)row * a.gstride;
+    const int cap = a.caps ? a.caps[(int64_t)b * a.cs + j - 1] : -1;
+    const int ghi = (cap >= 0 && cap < n) ? cap : n;
+    for (int t = tid; t < kc + kK3LPad; t += kK3Threads) {
+      const int k = k0 + t;
+      const bool in = k < k1;
+      sdp[t] = in ? ld_cg(gprev + k) : T::inf();   // produced by other CTAs / peers: read at L2
+      sL[t] = in ? gL[k] : (L)1;
+    }
+    const int s0 = c0 - k1 - kK3GPadLo;
+    for (int t = tid; t <= lay.gLen; t += kK3Threads) {
+      const int s = s0 + t;
+      const G g = (s >= 1 && s <= ghi) ? grow[s] : T::gpad();
+      if (t < lay.gLen) sG[t] = g;
+      if (t > 0) sG2[t - 1] = g;
+    }
+    __syncthreads();
+    const int cw = c0 + kWarpCols * warp;
+    if (cw <= imaxb) {
+      const int c = cw + kLaneCols * cl;
+      const int Q = 4 * ((k1 - k0 + 4 * kSplitLanes - 1) / (4 * kSplitLanes));
+      D acc[kLaneCols];
+      int arg[kLaneCols], klo[kLaneCols];
+#pragma unroll
+      for (int r = 0; r < kLaneCols; ++r) { acc[r] = T::inf(); arg[r] = -1; klo[r] = j - 1; }
+      sweep_slide<DT, SR, false, false, kLaneCols>(sL - k0, sdp - k0, sG + (c - s0), sG2 + (c - s0), k0 + kg * Q,
+                                                   Q / 4, acc, arg, klo);
+#pragma unroll
+      for (int off = kColLanes; off < 32; off <<= 1)
+#pragma unroll
+        for (int r = 0; r < kLaneCols; ++r) acc[r] = T::vmin(acc[r], __shfl_xor_sync(0xffffffffu, acc[r], off));
+      if (kg == 0) {
+#pragma unroll
+        for (int r = 0; r < kLaneCols; ++r) {
+          const int i = c + r;
+          if (i >= j && i <= imaxb) {
+            const D v = T::norm(acc[r]);
+            if (v != T::inf()) AtomicBits<D>::amin(gcur + i, v);
+          }
+        }
+      }
+    }
+    // ---- completion of the column block -> publish
+    __threadfence();
+    __syncthreads();
+    const int64_t bidx = ((int64_t)j * B + b) * ncb + blk;
+    if (tid == 0) {
+      s_flag = atomicAdd(pa.blk_done + bidx, 1u) == (unsigned)(nch - 1);
+      if (s_flag && pa.peer_dp) s_flag = wait_flag(pa.start_flag, pa.wait_start, pa.err) ? 1 : 2;
+    }
+    __syncthreads();
+    if (s_flag) {
+      __threadfence();
+      if (pa.peer_dp && s_flag == 1) {
+        const int64_t roff = ((int64_t)b * (m + 1) + j) * (n + 1);
+        const D* mine = reinterpret_cast<const D*>(a.dpws) + roff;
+        const int lo = max(c0, j), hi = imaxb;
+        for (int r = 0; r < pa.own_world; ++r) {
+          if (r == pa.own_rank) continue;
+          D* dst = reinterpret_cast<D*>(pa.peer_dp[r]) + roff;
+          for (int i = lo + tid; i <= hi; i += kK3Threads) dst[i] = ld_cg(mine + i);
+        }
+        __threadfence_system();
+        __syncthreads();
+        if (tid == 0)
+          for (int r = 0; r < pa.own_world; ++r)
+            if (r != pa.own_rank) atomicAdd_system(pa.peer_ready[r] + bidx, 1ull);
+      }
+      if (tid == 0) atomicAdd_system(pa.ready + bidx, 1ull);   // local consumers
+    }
+    __syncthreads();
+  }
+}
+
+// split mode: wait until the block holding column n of row m arrived for every valid problem
+__global__ void k5_wait_last(PersistArgs pa) {
+  const SolveArgs& a = pa.a;
+  const int n = a.n, m = a.m;
+  const int blk = (n - (m & ~3)) / kK3Cols;
+  for (int b = 0; b < a.B; ++b)
+    if (a.status[b] == HEDDLE_OK) wait_flag(pa.ready + ((int64_t)m * a.B + b) * pa.ncb + blk, pa.epoch, pa.err);
+  __threadfence();
 }
 
 // ---------------------------------------------------------------- fused exchange helpers

@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <new>
 #include <vector>
+#include <algorithm>
 
 #include "backtrack.cuh"
 #include "dp_batched.cuh"
@@ -85,6 +86,15 @@ struct heddle_place_ctx {
   unsigned int* d_blkdone = nullptr;          // [max_batch][ncb_max]
   int* d_err = nullptr;
   int64_t epoch = 0;                          // collective solves so far (same on every rank)
+  // persistent dataflow kernel (K5)
+  unsigned long long* d_ready = nullptr;      // [max_m+1][max_batch][ncb_max] per-block epoch counters
+  unsigned long long** d_peer_ready = nullptr; // device array [world]
+  std::vector<void*> peer_ready_h;
+  int4* d_tiles = nullptr;
+  size_t tiles_cap = 0;
+  int64_t tiles_n = 0;
+  int tiles_key[6] = {-1, -1, -1, -1, -1, -1};
+  int64_t ready_epoch = 0;                    // solves that used d_ready (single-GPU and split)
   std::vector<unsigned long long> expect;     // cumulative arrivals expected per counter
 };
 
@@ -132,6 +142,7 @@ K4Fn k4_for(int dt, int sr, bool kv) {
 }
 
 using K3Fn = void (*)(LayerArgs);
+using K5Fn = void (*)(PersistArgs);
 using KPro = void (*)(SolveArgs);
 template <int DT, int SR>
 K3Fn pick_k3(bool kp, bool kv) {
@@ -220,13 +231,151 @@ bool check_profile(const heddle_place_config* c, double* gmax) {
 // Batched (one CTA per problem) vs layered (all SMs per layer) -- rough cost model:
 // batched: waves x per-problem cells / (~12 cells/clk for one 4-warp CTA);
 // layered: all cells / (~30 cells/clk/SM x SMs) + per-layer launch/drain (~6000 clk).
+// layered (persistent dataflow): max(all cells / (~30 cells/clk/SM x SMs), critical path of m dependent
+// tiles of 512 columns x kc splits at ~11 cells/clk) -- see k5_kc().
+int k5_kc(int n, int m, int B, int num_sms) {
+  const double cells = (double)B * (double)heddle_place_transitions(n, m);
+  const double work = cells / (30.0 * num_sms);
+  int kc = 2048;
+  while (kc > 256 && (double)m * kK3Cols * std::min(kc, n) / 11.0 > 0.25 * work) kc /= 2;
+  return kc;
+}
 bool use_layered(const heddle_place_ctx* x, int n, int m, int B) {
   const double cells = (double)heddle_place_transitions(n, m);
   const double slots = (double)x->num_sms * 8.0;
   const double waves = std::ceil((double)B / slots);
   const double t2 = waves * cells / 12.0;
-  const double t3 = (double)B * cells / (30.0 * x->num_sms) + (double)(m - 1) * 6000.0;
+  const int kc = k5_kc(n, m, B, x->num_sms);
+  const double t3 = std::max((double)B * cells / (30.0 * x->num_sms), (double)m * kK3Cols * std::min(kc, n) / 11.0) +
+                    20000.0;
   return t3 < t2;
+}
+
+template <int DT, int SR>
+K5Fn pick_k5() { return k5_persistent<DT, SR>; }
+
+// K5 (persistent dataflow over all layers); fill + prologue have been enqueued already.
+heddle_status solve_persistent(heddle_place_ctx* x, SolveArgs& a, cudaStream_t s) {
+  const int dt = x->dtype, sr = x->semiring;
+  const int n = a.n, m = a.m, B = a.B, world = x->split_world, rank = x->split_rank;
+  const int kc = k5_kc(n, m, B, x->num_sms);
+  const int ncb = (n - m + 3) / kK3Cols + 1;
+  const int ncb_max = (x->max_n + 3) / kK3Cols + 2;
+  if (!x->d_ready) {
+    const size_t bytes = 8 * (size_t)(x->max_m + 1) * x->max_batch * ncb_max;
+    if (cudaMalloc(&x->d_ready, bytes) != cudaSuccess || cudaMemset(x->d_ready, 0, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return HEDDLE_E_NOMEM;
+    }
+  }
+  if (!x->d_blkdone) {
+    if (cudaMalloc(&x->d_blkdone, sizeof(unsigned) * (size_t)x->max_batch * ncb_max * (x->max_m + 1)) != cudaSuccess) {
+      cudaGetLastError();
+      return HEDDLE_E_NOMEM;
+    }
+  }
+  if (!x->d_err) {
+    if (cudaMalloc(&x->d_err, sizeof(int)) != cudaSuccess || cudaMemset(x->d_err, 0, sizeof(int)) != cudaSuccess) {
+      cudaGetLastError();
+      return HEDDLE_E_NOMEM;
+    }
+  }
+  // tile list (layer-major, chunk-major inside a layer; this rank's blocks only), cached per shape
+  const int key[6] = {n, m, kc, rank, world, ncb};
+  if (std::memcmp(key, x->tiles_key, sizeof(key)) != 0) {
+    std::vector<int4> tl;
+    const int nown = owned_slots(ncb, world);
+    for (int j = 2; j <= m; ++j) {
+      const int cbase = j & ~3, kstart = (j - 1) & ~3, imax = n - m + j;
+      int qmax = 0;
+      std::vector<std::pair<int, int>> blks;   // (blk, nch)
+      for (int sl = 0; sl < nown; ++sl) {
+        const int blk = owned_block(sl, rank, world);
+        const int c0 = cbase + kK3Cols * blk;
+        if (blk >= ncb || c0 > imax || (j == m && c0 + kK3Cols <= n)) continue;
+        const int kend = align4(std::min(c0 + kK3Cols - 1, imax));
+        const int nch = (kend - kstart + kc - 1) / kc;
+        blks.push_back({blk, nch});
+        qmax = std::max(qmax, nch);
+      }
+      std::sort(blks.begin(), blks.end());
+      for (int q = 0; q < qmax; ++q)
+        for (auto& bn : blks)
+          if (q < bn.second) tl.push_back(make_int4(j, bn.first, q, bn.second));
+    }
+    if (tl.size() > x->tiles_cap) {
+      cudaFree(x->d_tiles);
+      x->d_tiles = nullptr;
+      x->tiles_cap = 0;
+      if (cudaMalloc(&x->d_tiles, sizeof(int4) * tl.size()) != cudaSuccess) { cudaGetLastError(); return HEDDLE_E_NOMEM; }
+      x->tiles_cap = tl.size();
+    }
+    if (!tl.empty() && cudaMemcpy(x->d_tiles, tl.data(), sizeof(int4) * tl.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+      return HEDDLE_E_CUDA;
+    x->tiles_n = (int64_t)tl.size();
+    std::memcpy(x->tiles_key, key, sizeof(key));
+  }
+  x->ready_epoch++;
+  if (cudaMemsetAsync(x->d_ctr, 0, 8, s) != cudaSuccess ||
+      cudaMemsetAsync(x->d_blkdone, 0, sizeof(unsigned) * (size_t)B * ncb * (m + 1), s) != cudaSuccess)
+    return HEDDLE_E_CUDA;
+  PersistArgs pa{};
+  pa.a = a;
+  pa.kc = kc;
+  pa.ncb = ncb;
+  pa.tiles = x->d_tiles;
+  pa.nentries = x->tiles_n;
+  pa.counter = x->d_ctr;
+  pa.blk_done = x->d_blkdone;
+  pa.ready = x->d_ready;
+  pa.epoch = (unsigned long long)x->ready_epoch;
+  pa.own_rank = rank;
+  pa.own_world = world;
+  pa.err = x->d_err;
+  if (world > 1) {
+    x->epoch++;
+    if ((int)x->expect.size() < x->max_m + 1) x->expect.assign(x->max_m + 1, 0ull);
+    x->expect[0] += (unsigned long long)(world - 1);
+    k3_signal_start<<<1, 1, 0, s>>>(x->d_peer_flags, rank, world);
+    x->launches++;
+    pa.peer_dp = x->d_peer_dp;
+    pa.peer_ready = x->d_peer_ready;
+    pa.start_flag = x->d_flags;
+    pa.wait_start = x->expect[0];
+    pa.a.err = x->d_err;
+    a.err = x->d_err;
+  }
+  K5Fn fn = HP_DISPATCH(pick_k5);
+  const int smem = k3_smem(dt, sr, kc);
+  int occ = 0;
+  cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kK3Threads, smem);
+  if (occ < 1) return HEDDLE_E_CUDA;
+  const int64_t ntiles = x->tiles_n * B;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)occ * x->num_sms));
+  std::vector<cudaEvent_t> tev(2);
+  if (x->trace) {
+    for (auto& e : tev) cudaEventCreate(&e);
+    cudaEventRecord(tev[0], s);
+  }
+  fn<<<grid, kK3Threads, smem, s>>>(pa);
+  x->launches++;
+  if (world > 1) {
+    k5_wait_last<<<1, 1, 0, s>>>(pa);
+    x->launches++;
+  }
+  if (x->trace) {
+    cudaEventRecord(tev[1], s);
+    cudaStreamSynchronize(s);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, tev[0], tev[1]);
+    std::fprintf(stderr, "[heddle_place trace] persistent rank %d/%d n=%d m=%d B=%d kc=%d grid=%d tiles=%lld: %.3f ms\n",
+                 rank, world, n, m, B, kc, grid, (long long)ntiles, ms);
+    for (auto& e : tev) cudaEventDestroy(e);
+  }
+  HP_DISPATCH(finalize_launch, a, s);
+  x->launches++;
+  return cudaGetLastError() == cudaSuccess ? HEDDLE_OK : HEDDLE_E_CUDA;
 }
 
 heddle_status solve_layered(heddle_place_ctx* x, SolveArgs& a, bool kp, bool kv, cudaStream_t s) {
@@ -249,6 +398,9 @@ heddle_status solve_layered(heddle_place_ctx* x, SolveArgs& a, bool kp, bool kv,
   HP_DISPATCH(fill_launch, a, cells, fill_grid, s);
   pro_for(dt, sr, kp, kv)<<<B, 256, 0, s>>>(a);
   x->launches += 2;
+  const char* nok5 = std::getenv("HEDDLE_PLACE_NO_PERSISTENT");
+  if (!kp && !kv && !(x->split_world > 1 && (x->split_emulate || !x->p2p)) && !(nok5 && nok5[0] == '1'))
+    return solve_persistent(x, a, s);
   // tile geometry: 256 columns x kc splits; kc sized for >= ~4 tiles per resident CTA
   // (per rank in split mode: each rank computes 1/world of the layer's cells)
   const double layer_cells = (double)B * (double)(n - m + 1) * (double)(n - m + 2) / 2.0 / x->split_world;
@@ -449,8 +601,13 @@ void heddle_place_destroy(heddle_place_ctx* ctx) {
     if ((int)r != ctx->split_rank && ctx->peer_dp_h[r]) cudaIpcCloseMemHandle(ctx->peer_dp_h[r]);
   for (size_t r = 0; r < ctx->peer_flags_h.size(); ++r)
     if ((int)r != ctx->split_rank && ctx->peer_flags_h[r]) cudaIpcCloseMemHandle(ctx->peer_flags_h[r]);
+  for (size_t r = 0; r < ctx->peer_ready_h.size(); ++r)
+    if ((int)r != ctx->split_rank && ctx->peer_ready_h[r]) cudaIpcCloseMemHandle(ctx->peer_ready_h[r]);
   cudaFree(ctx->d_peer_dp);
   cudaFree(ctx->d_peer_flags);
+  cudaFree(ctx->d_peer_ready);
+  cudaFree(ctx->d_ready);
+  cudaFree(ctx->d_tiles);
   cudaFree(ctx->d_flags);
   cudaFree(ctx->d_blkdone);
   cudaFree(ctx->d_err);
@@ -738,12 +895,16 @@ static heddle_status setup_p2p(heddle_place_ctx* x) {
       cudaMalloc(&x->d_blkdone, sizeof(unsigned) * (size_t)x->max_batch * ncb_max * (x->max_m + 1)) != cudaSuccess ||
       cudaMalloc(&x->d_err, sizeof(int)) != cudaSuccess || cudaMemset(x->d_err, 0, sizeof(int)) != cudaSuccess ||
       cudaMalloc(&x->d_peer_dp, sizeof(void*) * world) != cudaSuccess ||
-      cudaMalloc(&x->d_peer_flags, sizeof(void*) * world) != cudaSuccess) {
+      cudaMalloc(&x->d_peer_flags, sizeof(void*) * world) != cudaSuccess ||
+      cudaMalloc(&x->d_peer_ready, sizeof(void*) * world) != cudaSuccess ||
+      (!x->d_ready && (cudaMalloc(&x->d_ready, 8 * (size_t)(x->max_m + 1) * x->max_batch * ncb_max) != cudaSuccess ||
+                       cudaMemset(x->d_ready, 0, 8 * (size_t)(x->max_m + 1) * x->max_batch * ncb_max) != cudaSuccess))) {
     cudaGetLastError();
     return HEDDLE_E_NOMEM;
   }
-  cudaIpcMemHandle_t mine[2];
-  if (cudaIpcGetMemHandle(&mine[0], x->d_dp) != cudaSuccess || cudaIpcGetMemHandle(&mine[1], x->d_flags) != cudaSuccess) {
+  cudaIpcMemHandle_t mine[3];
+  if (cudaIpcGetMemHandle(&mine[0], x->d_dp) != cudaSuccess || cudaIpcGetMemHandle(&mine[1], x->d_flags) != cudaSuccess ||
+      cudaIpcGetMemHandle(&mine[2], x->d_ready) != cudaSuccess) {
     cudaGetLastError();
     return HEDDLE_OK;   // no IPC: keep the NCCL exchange
   }
@@ -752,7 +913,7 @@ static heddle_status setup_p2p(heddle_place_ctx* x) {
   if (cudaMalloc(&dsend, hb) != cudaSuccess || cudaMalloc(&drecv, hb * world) != cudaSuccess) return HEDDLE_E_NOMEM;
   cudaMemcpy(dsend, mine, hb, cudaMemcpyHostToDevice);
   ncclResult_t nr = ncclAllGather(dsend, drecv, hb, ncclChar, x->comm, 0);
-  std::vector<cudaIpcMemHandle_t> all(2 * world);
+  std::vector<cudaIpcMemHandle_t> all(3 * world);
   if (nr == ncclSuccess) cudaMemcpy(all.data(), drecv, hb * world, cudaMemcpyDeviceToHost);
   cudaFree(dsend);
   cudaFree(drecv);
@@ -763,14 +924,17 @@ static heddle_status setup_p2p(heddle_place_ctx* x) {
   cudaGetDeviceCount(&ndev);
   x->peer_dp_h.assign(world, nullptr);
   x->peer_flags_h.assign(world, nullptr);
+  x->peer_ready_h.assign(world, nullptr);
   for (int r = 0; r < world && ok; ++r) {
     if (r == rank) {
       x->peer_dp_h[r] = x->d_dp;
       x->peer_flags_h[r] = x->d_flags;
+      x->peer_ready_h[r] = x->d_ready;
       continue;
     }
-    if (cudaIpcOpenMemHandle(&x->peer_dp_h[r], all[2 * r], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
-        cudaIpcOpenMemHandle(&x->peer_flags_h[r], all[2 * r + 1], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+    if (cudaIpcOpenMemHandle(&x->peer_dp_h[r], all[3 * r], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
+        cudaIpcOpenMemHandle(&x->peer_flags_h[r], all[3 * r + 1], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
+        cudaIpcOpenMemHandle(&x->peer_ready_h[r], all[3 * r + 2], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
       cudaGetLastError();
       ok = 0;
     }
@@ -787,13 +951,16 @@ static heddle_status setup_p2p(heddle_place_ctx* x) {
       if (r == rank) continue;
       if (x->peer_dp_h[r]) cudaIpcCloseMemHandle(x->peer_dp_h[r]);
       if (x->peer_flags_h[r]) cudaIpcCloseMemHandle(x->peer_flags_h[r]);
+      if (x->peer_ready_h[r]) cudaIpcCloseMemHandle(x->peer_ready_h[r]);
     }
     x->peer_dp_h.clear();
     x->peer_flags_h.clear();
+    x->peer_ready_h.clear();
     return HEDDLE_OK;
   }
   cudaMemcpy(x->d_peer_dp, x->peer_dp_h.data(), sizeof(void*) * world, cudaMemcpyHostToDevice);
   cudaMemcpy(x->d_peer_flags, x->peer_flags_h.data(), sizeof(void*) * world, cudaMemcpyHostToDevice);
+  cudaMemcpy(x->d_peer_ready, x->peer_ready_h.data(), sizeof(void*) * world, cudaMemcpyHostToDevice);
   x->p2p = cudaGetLastError() == cudaSuccess;
   return HEDDLE_OK;
 }
