@@ -55,6 +55,31 @@ __global__ void __launch_bounds__(32 * kK4Warps) k4_backtrack(SolveArgs a, int32
         lo = l;
       }
     }
+    // The group cost c(k) = L[k] * G_j(cur - k) is non-increasing in k (L sorted, F non-decreasing,
+    // caps only remove low k), and every candidate satisfies v(k) >= c(k) (dp >= 0), so the lowest
+    // argmin lies at or after the first k with c(k) <= target: find it by a 32-ary search.
+    {
+      int a0 = lo, b0 = cur;   // first k in [a0, b0) with c(k) <= target; b0 = none
+      while (b0 - a0 > 32) {
+        const int step = (b0 - a0 + 31) / 32;
+        const int k = a0 + lane * step;
+        const bool ok = k < b0 && T::norm(T::comb(T::zero(), gL[k], grow[cur - k])) <= target;
+        const unsigned msk = __ballot_sync(0xffffffffu, ok);
+        if (msk == 0) { a0 = min(b0, a0 + 31 * step + 1); continue; }
+        const int t = __ffs(msk) - 1;
+        if (t == 0) { b0 = a0; break; }
+        const int na = a0 + (t - 1) * step + 1;
+        b0 = a0 + t * step;
+        a0 = na;
+      }
+      if (b0 - a0 > 0) {
+        const int k = a0 + lane;
+        const bool ok = k < b0 && T::norm(T::comb(T::zero(), gL[k], grow[cur - k])) <= target;
+        const unsigned msk = __ballot_sync(0xffffffffu, ok);
+        b0 = msk ? a0 + __ffs(msk) - 1 : b0;
+      }
+      lo = b0;
+    }
     int found = -1;
     for (int base = lo; base < cur && found < 0; base += 32) {
       const int k = base + lane;
