@@ -13,6 +13,57 @@ namespace hp {
 
 constexpr int kK4Warps = 8;
 
+// The group cost c(k) = L[k] * G_j(cur - k) is non-increasing in k (L sorted, F non-decreasing,
+// caps only remove low k), and every candidate satisfies v(k) >= c(k) (dp >= 0), so the lowest
+// argmin lies at or after the first k in [lo, cur) with c(k) <= target: a warp-wide 32-ary search.
+template <int DT, int SR>
+__device__ int first_within_target(const typename Tr<DT, SR>::L* __restrict__ gL,
+                                   const typename Tr<DT, SR>::G* __restrict__ grow, int lo, int cur,
+                                   typename Tr<DT, SR>::D target, int lane) {
+  using T = Tr<DT, SR>;
+  int a0 = lo, b0 = cur;   // first k in [a0, b0) with c(k) <= target; b0 = none
+  while (b0 - a0 > 32) {
+    const int step = (b0 - a0 + 31) / 32;
+    const int k = a0 + lane * step;
+    const bool ok = k < b0 && T::norm(T::comb(T::zero(), gL[k], grow[cur - k])) <= target;
+    const unsigned msk = __ballot_sync(0xffffffffu, ok);
+    if (msk == 0) { a0 = min(b0, a0 + 31 * step + 1); continue; }
+    const int t = __ffs(msk) - 1;
+    if (t == 0) { b0 = a0; break; }
+    const int na = a0 + (t - 1) * step + 1;
+    b0 = a0 + t * step;
+    a0 = na;
+  }
+  if (b0 - a0 > 0) {
+    const int k = a0 + lane;
+    const bool ok = k < b0 && T::norm(T::comb(T::zero(), gL[k], grow[cur - k])) <= target;
+    const unsigned msk = __ballot_sync(0xffffffffu, ok);
+    b0 = msk ? a0 + __ffs(msk) - 1 : b0;
+  }
+  return b0;
+}
+
+// lower split bound of layer j's group ending at cur: j-1, the size cap, the kv cap (R6)
+template <int DT, bool KV>
+__device__ int split_lower_bound(const SolveArgs& a, int b, int j, int cur, const typename SpT<DT>::type* gSp) {
+  using S = typename SpT<DT>::type;
+  int lo = j - 1;
+  const int cap = a.caps ? a.caps[(int64_t)b * a.cs + j - 1] : -1;
+  if (cap >= 0) lo = max(lo, cur - cap);
+  if constexpr (KV) {
+    const int64_t kvc = a.kv[(int64_t)b * a.kvs + j - 1];
+    if (kvc >= 0) {
+      int l = lo, h = cur;   // smallest k with Sp[cur] - Sp[k] <= kv (monotone in k)
+      while (l < h) {
+        const int mid = (l + h) >> 1;
+        if (gSp[cur] - gSp[mid] <= (S)kvc) h = mid; else l = mid + 1;
+      }
+      lo = l;
+    }
+  }
+  return lo;
+}
+
 template <int DT, int SR, bool KV>
 __global__ void __launch_bounds__(32 * kK4Warps) k4_backtrack(SolveArgs a, int32_t* bounds) {
   using T = Tr<DT, SR>;
@@ -41,45 +92,8 @@ __global__ void __launch_bounds__(32 * kK4Warps) k4_backtrack(SolveArgs a, int32
     int row = 0;
     for (int q = 0; q < a.D; ++q) row = (a.prof_deg[q] == d) ? q : row;
     const G* grow = gtab + (int64_t)row * a.gstride;
-    int lo = j - 1;
-    const int cap = a.caps ? a.caps[(int64_t)b * a.cs + j - 1] : -1;
-    if (cap >= 0) lo = max(lo, cur - cap);
-    if constexpr (KV) {
-      const int64_t kvc = a.kv[(int64_t)b * a.kvs + j - 1];
-      if (kvc >= 0) {
-        int l = lo, h = cur;   // smallest k with Sp[cur] - Sp[k] <= kv (monotone in k)
-        while (l < h) {
-          int mid = (l + h) >> 1;
-          if (gSp[cur] - gSp[mid] <= (S)kvc) h = mid; else l = mid + 1;
-        }
-        lo = l;
-      }
-    }
-    // The group cost c(k) = L[k] * G_j(cur - k) is non-increasing in k (L sorted, F non-decreasing,
-    // caps only remove low k), and every candidate satisfies v(k) >= c(k) (dp >= 0), so the lowest
-    // argmin lies at or after the first k with c(k) <= target: find it by a 32-ary search.
-    {
-      int a0 = lo, b0 = cur;   // first k in [a0, b0) with c(k) <= target; b0 = none
-      while (b0 - a0 > 32) {
-        const int step = (b0 - a0 + 31) / 32;
-        const int k = a0 + lane * step;
-        const bool ok = k < b0 && T::norm(T::comb(T::zero(), gL[k], grow[cur - k])) <= target;
-        const unsigned msk = __ballot_sync(0xffffffffu, ok);
-        if (msk == 0) { a0 = min(b0, a0 + 31 * step + 1); continue; }
-        const int t = __ffs(msk) - 1;
-        if (t == 0) { b0 = a0; break; }
-        const int na = a0 + (t - 1) * step + 1;
-        b0 = a0 + t * step;
-        a0 = na;
-      }
-      if (b0 - a0 > 0) {
-        const int k = a0 + lane;
-        const bool ok = k < b0 && T::norm(T::comb(T::zero(), gL[k], grow[cur - k])) <= target;
-        const unsigned msk = __ballot_sync(0xffffffffu, ok);
-        b0 = msk ? a0 + __ffs(msk) - 1 : b0;
-      }
-      lo = b0;
-    }
+    int lo = split_lower_bound<DT, KV>(a, b, j, cur, gSp);
+    lo = first_within_target<DT, SR>(gL, grow, lo, cur, target, lane);
     int found = -1;
     for (int base = lo; base < cur && found < 0; base += 32) {
       const int k = base + lane;
@@ -96,6 +110,71 @@ __global__ void __launch_bounds__(32 * kK4Warps) k4_backtrack(SolveArgs a, int32
     if (lane == 0) out[j - 1] = cur;
   }
   if (lane == 0) out[0] = 0;
+}
+
+// One CTA (kK4CtaThreads threads) per problem: for few, large problems (n = 65536), where the
+// lowest-argmin scan of min-plus can cover tens of thousands of splits per layer.
+constexpr int kK4CtaThreads = 512;
+constexpr int kK4PerThread = 8;
+
+template <int DT, int SR, bool KV>
+__global__ void __launch_bounds__(kK4CtaThreads) k4_backtrack_cta(SolveArgs a, int32_t* bounds) {
+  using T = Tr<DT, SR>;
+  using L = typename T::L;
+  using G = typename T::G;
+  using D = typename T::D;
+  using S = typename SpT<DT>::type;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int b = blockIdx.x;
+  const int n = a.n, m = a.m;
+  int32_t* out = bounds + (int64_t)b * (m + 1);
+  if (a.status[b] != HEDDLE_OK) {
+    for (int j = tid; j <= m; j += kK4CtaThreads) out[j] = -1;
+    return;
+  }
+  __shared__ int s_lo, s_found, s_row;
+  const L* gL = reinterpret_cast<const L*>(a.lengths) + (int64_t)b * a.ls;
+  const D* gdp = reinterpret_cast<const D*>(a.dpws) + (int64_t)b * (m + 1) * (n + 1);
+  const G* gtab = reinterpret_cast<const G*>(a.gtab);
+  const S* gSp = KV ? reinterpret_cast<const S*>(a.spws) + (int64_t)b * (n + 1) : nullptr;
+  int cur = n;
+  if (tid == 0) out[m] = n;
+  for (int j = m; j >= 2; --j) {
+    const D target = gdp[(int64_t)j * (n + 1) + cur];
+    if (warp == 0) {
+      const int d = a.degrees[(int64_t)b * a.ds + j - 1];
+      int row = 0;
+      for (int q = 0; q < a.D; ++q) row = (a.prof_deg[q] == d) ? q : row;
+      const G* grow = gtab + (int64_t)row * a.gstride;
+      int lo = split_lower_bound<DT, KV>(a, b, j, cur, gSp);
+      lo = first_within_target<DT, SR>(gL, grow, lo, cur, target, lane);
+      if (lane == 0) { s_lo = lo; s_row = row; s_found = INT_MAX; }
+    }
+    __syncthreads();
+    const G* grow = gtab + (int64_t)s_row * a.gstride;
+    const D* prev = gdp + (int64_t)(j - 1) * (n + 1);
+    for (int base = s_lo; base < cur; base += kK4CtaThreads * kK4PerThread) {
+      int mine = INT_MAX;
+#pragma unroll
+      for (int i = 0; i < kK4PerThread; ++i) {
+        const int k = base + i * kK4CtaThreads + tid;
+        if (mine == INT_MAX && k < cur && T::norm(T::comb(prev[k], gL[k], grow[cur - k])) == target) mine = k;
+      }
+      mine = __reduce_min_sync(0xffffffffu, mine);
+      if (lane == 0 && mine != INT_MAX) atomicMin(&s_found, mine);
+      __syncthreads();
+      if (s_found != INT_MAX) break;
+    }
+    const int found = s_found;
+    __syncthreads();
+    if (found == INT_MAX) {   // unreachable: the target is one of these candidates
+      for (int q = tid; q <= m; q += kK4CtaThreads) out[q] = -1;
+      return;
+    }
+    cur = found;
+    if (tid == 0) out[j - 1] = cur;
+  }
+  if (tid == 0) out[0] = 0;
 }
 
 }  // namespace hp

@@ -191,16 +191,29 @@ __device__ __forceinline__ void sweep_slide(const typename Tr<DT, SR>::L* __rest
       typename T::L lv[4];
       ld4(sdp + k, dpv);
       ld4(sL + k, lv);
+      if constexpr (!KP) {
+        // all 4R candidates first, then pairwise 3-input minima (FMNMX3 / VIMNMX3)
+        typename T::D v[4][R];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            v[u][r] = T::comb(dpv[u], lv[u], w[r - u + 3]);
+            if (MASKED) v[u][r] = (k + u >= klo[r]) ? v[u][r] : T::inf();
+          }
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          typename T::D v = T::comb(dpv[u], lv[u], w[r - u + 3]);
-          if (MASKED) v = (k + u >= klo[r]) ? v : T::inf();
-          if (KP) {
+          acc[r] = T::vmin(T::vmin(acc[r], v[0][r]), v[1][r]);
+          acc[r] = T::vmin(T::vmin(acc[r], v[2][r]), v[3][r]);
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            typename T::D v = T::comb(dpv[u], lv[u], w[r - u + 3]);
+            if (MASKED) v = (k + u >= klo[r]) ? v : T::inf();
             if (v < acc[r]) { acc[r] = v; arg[r] = k + u; }   // strict '<', ascending k: lowest index
-          } else {
-            acc[r] = T::vmin(acc[r], v);
           }
         }
       }

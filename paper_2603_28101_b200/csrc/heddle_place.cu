@@ -129,6 +129,10 @@ template <int DT, int SR>
 K4Fn pick_k4(bool kv) {
   return kv ? k4_backtrack<DT, SR, true> : k4_backtrack<DT, SR, false>;
 }
+template <int DT, int SR>
+K4Fn pick_k4c(bool kv) {
+  return kv ? k4_backtrack_cta<DT, SR, true> : k4_backtrack_cta<DT, SR, false>;
+}
 
 K2Fn k2_for(int dt, int sr, bool kp, bool kv) {
   if (dt == HEDDLE_F32) return sr == HEDDLE_MINMAX ? pick_k2<HEDDLE_F32, HEDDLE_MINMAX>(kp, kv) : pick_k2<HEDDLE_F32, HEDDLE_MINPLUS>(kp, kv);
@@ -162,6 +166,7 @@ KPro pick_pro(bool kp, bool kv) {
                       : (sr == HEDDLE_MINMAX ? NAME<HEDDLE_U32, HEDDLE_MINMAX>(__VA_ARGS__)             \
                                              : NAME<HEDDLE_U32, HEDDLE_MINPLUS>(__VA_ARGS__)))
 K3Fn k3_for(int dt, int sr, bool kp, bool kv) { return HP_DISPATCH(pick_k3, kp, kv); }
+K4Fn k4c_for(int dt, int sr, bool kv) { return HP_DISPATCH(pick_k4c, kv); }
 KPro pro_for(int dt, int sr, bool kp, bool kv) { return HP_DISPATCH(pick_pro, kp, kv); }
 template <int DT, int SR> int k3_smem_t(int kc) { return K3Smem<DT, SR>(kc).total; }
 int k3_smem(int dt, int sr, int kc) { return HP_DISPATCH(k3_smem_t, kc); }
@@ -795,7 +800,12 @@ heddle_status heddle_place_backtrack(heddle_place_ctx* x, int32_t* boundaries_ou
   DeviceGuard guard(x->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const SolveArgs& a = x->last;
-  k4_for(x->dtype, x->semiring, x->last_kv)<<<(a.B + kK4Warps - 1) / kK4Warps, 32 * kK4Warps, 0, s>>>(a, boundaries_out);
+  // few min-plus problems: a CTA per problem (the cost bound prunes little there, so the
+  // lowest-argmin scan can cover tens of thousands of splits per layer at large n)
+  if (a.B < x->num_sms && x->semiring == HEDDLE_MINPLUS)
+    k4c_for(x->dtype, x->semiring, x->last_kv)<<<a.B, kK4CtaThreads, 0, s>>>(a, boundaries_out);
+  else
+    k4_for(x->dtype, x->semiring, x->last_kv)<<<(a.B + kK4Warps - 1) / kK4Warps, 32 * kK4Warps, 0, s>>>(a, boundaries_out);
   x->launches++;
   if (cudaGetLastError() != cudaSuccess) return HEDDLE_E_CUDA;
   if (parents_out) {
