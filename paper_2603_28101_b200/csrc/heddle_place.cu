@@ -238,8 +238,8 @@ bool check_profile(const heddle_place_config* c, double* gmax) {
 // layered: all cells / (~30 cells/clk/SM x SMs) + per-layer launch/drain (~6000 clk).
 // layered (persistent dataflow): max(all cells / (~30 cells/clk/SM x SMs), critical path of m dependent
 // tiles of 512 columns x kc splits at ~11 cells/clk) -- see k5_kc().
-int k5_kc(int n, int m, int B, int num_sms) {
-  const double cells = (double)B * (double)heddle_place_transitions(n, m);
+int k5_kc(int n, int m, int B, int num_sms, int world = 1) {
+  const double cells = (double)B * (double)heddle_place_transitions(n, m) / world;   // this rank's share
   const double work = cells / (30.0 * num_sms);
   int kc = 2048;
   while (kc > 256 && (double)m * kK3Cols * std::min(kc, n) / 11.0 > 0.25 * work) kc /= 2;
@@ -263,7 +263,7 @@ K5Fn pick_k5() { return k5_persistent<DT, SR>; }
 heddle_status solve_persistent(heddle_place_ctx* x, SolveArgs& a, cudaStream_t s) {
   const int dt = x->dtype, sr = x->semiring;
   const int n = a.n, m = a.m, B = a.B, world = x->split_world, rank = x->split_rank;
-  const int kc = k5_kc(n, m, B, x->num_sms);
+  const int kc = k5_kc(n, m, B, x->num_sms, world);
   const int ncb = (n - m + 3) / kK3Cols + 1;
   const int ncb_max = (x->max_n + 3) / kK3Cols + 2;
   if (!x->d_ready) {
