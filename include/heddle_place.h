@@ -184,6 +184,10 @@ heddle_status heddle_place_init_split(const heddle_place_config* cfg, const void
                                       int32_t world, heddle_place_ctx** out);
 int32_t heddle_place_split_blocks(int32_t ncb, int32_t world, int32_t rank, int32_t* blocks_out, int32_t cap);
 
+/* Debug builds only (compiled with -DHEDDLE_CHECK_BOUNDS): number of shared-memory index-range
+ * violations the kernels detected so far on the current device; -1 in release builds. */
+int64_t heddle_place_debug_violations(void);
+
 void heddle_place_destroy(heddle_place_ctx* ctx);
 const char* heddle_place_strerror(heddle_status s);
 

@@ -73,6 +73,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_checked(out: str) -> str:
+    """Debug build with shared-memory bounds checks (-DHEDDLE_CHECK_BOUNDS)."""
+    cmd = [NVCC, *ARCH, *FLAGS, "-DHEDDLE_CHECK_BOUNDS", "-I", INCLUDE, "-shared", "-o", out, *sources(), *NCCL_FLAGS]
+    subprocess.check_call(cmd)
+    return out
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose=True)
     print(LIB)

@@ -72,6 +72,24 @@ struct SolveArgs {
 
 __host__ __device__ inline int align4(int x) { return (x + 3) & ~3; }
 
+// Debug builds (-DHEDDLE_CHECK_BOUNDS) verify, once per warp task / tile, that every shared-
+// memory index the sweep will touch lies inside its array, and count violations in a device
+// global (heddle_place_debug_violations()).  compute-sanitizer is not available on the pool.
+#ifdef HEDDLE_CHECK_BOUNDS
+__device__ unsigned long long g_hp_violations;
+#define HP_CHECK(cond) do { if (!(cond)) atomicAdd(&g_hp_violations, 1ull); } while (0)
+#else
+#define HP_CHECK(cond) do { } while (0)
+#endif
+
+// index range touched by sweep_slide for a lane: splits [kq, kq + 4*iters) plus the prefetch of
+// the window after the last step; G window indices relative to gcol: [-(k_last + 4) - 3, -kq + R]
+__device__ __forceinline__ void check_sweep(int kq, int iters, int R, int sdp_lo, int sdp_hi, int g_lo, int g_hi,
+                                            int gbase) {
+  HP_CHECK(kq >= sdp_lo && kq + 4 * iters + 3 < sdp_hi);
+  HP_CHECK(gbase - (kq + 4 * iters) - 3 >= g_lo && gbase - kq + R + 3 < g_hi);
+}
+
 // Shared-memory carve-up (bytes), identical on host and device.
 template <int DT, int SR>
 struct K2Smem {
@@ -414,6 +432,8 @@ __global__ void __launch_bounds__(kK2Threads) k2_dp_batched(SolveArgs a) {
 #pragma unroll
           for (int r = 0; r < kLaneCols; ++r) klo[r] = sklo[min(max(c + r, j), imax)];
         }
+        check_sweep(kstart + kg * Q, Q / 4, kLaneCols, 0, align4(n + kLPad), 0, align4(kGPad + n + kGTail + 1),
+                    kGPad + c);
         sweep_slide<DT, SR, KP, KV, kLaneCols>(sL, prev, sG + kGPad + c, sG2 + kGPad + c, kstart + kg * Q, Q / 4,
                                                acc, arg, klo);
         // combine the kSplitLanes partial minima of each column (lowest split on ties)

@@ -391,6 +391,7 @@ __global__ void __launch_bounds__(kK3Threads) k3_layer(LayerArgs la) {
         for (int r = 0; r < kLaneCols; ++r) klo[r] = la.klo[(int64_t)b * (n + 1) + min(max(c + r, j), imaxb)];
       }
       // shifted bases: sdpb[k] = sdp[k - k0]; gcol - k - 3 = &G(c - k - 3)
+      check_sweep(k0 + kg * Q - k0, Q / 4, kLaneCols, 0, kc + kK3LPad, 0, lay.gLen, c - s0 - k0);
       sweep_slide<DT, SR, KP, KV, kLaneCols>(sL - k0, sdp - k0, sG + (c - s0), sG2 + (c - s0), k0 + kg * Q, Q / 4,
                                              acc, arg, klo);
 #pragma unroll
@@ -566,6 +567,7 @@ __global__ void __launch_bounds__(kK3Threads) k5_persistent(PersistArgs pa) {
       int arg[kLaneCols], klo[kLaneCols];
 #pragma unroll
       for (int r = 0; r < kLaneCols; ++r) { acc[r] = T::inf(); arg[r] = -1; klo[r] = j - 1; }
+      check_sweep(kg * Q, Q / 4, kLaneCols, 0, kc + kK3LPad, 0, lay.gLen, c - s0 - k0);
       sweep_slide<DT, SR, false, false, kLaneCols>(sL - k0, sdp - k0, sG + (c - s0), sG2 + (c - s0), k0 + kg * Q,
                                                    Q / 4, acc, arg, klo);
 #pragma unroll

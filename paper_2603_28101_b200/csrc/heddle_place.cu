@@ -1029,4 +1029,15 @@ int32_t heddle_place_split_blocks(int32_t ncb, int32_t world, int32_t rank, int3
   return cnt;
 }
 
+
+int64_t heddle_place_debug_violations(void) {
+#ifdef HEDDLE_CHECK_BOUNDS
+  unsigned long long v = 0;
+  if (cudaMemcpyFromSymbol(&v, g_hp_violations, sizeof(v)) != cudaSuccess) return -2;
+  return (int64_t)v;
+#else
+  return -1;
+#endif
+}
+
 }  // extern "C"

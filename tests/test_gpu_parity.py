@@ -315,3 +315,21 @@ def test_split_multi_gpu_torchrun():
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=root)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "SPLIT OK" in r.stdout
+
+
+def test_bounds_checked_build():
+    """Every kernel path on a debug build whose kernels verify the shared-memory index range of
+    each warp task / tile (compute-sanitizer is not available on the pool): zero violations."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+    from paper_2603_28101_b200 import _build
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib = os.path.join(tempfile.mkdtemp(), "libheddle_place_checked.so")
+    _build.build_checked(lib)
+    env = dict(os.environ, HEDDLE_PLACE_LIB=lib)
+    r = subprocess.run([sys.executable, os.path.join(root, "tests", "sanitize_run.py")], env=env, cwd=root,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "bounds violations: 0" in r.stdout, r.stdout[-2000:]
