@@ -220,3 +220,12 @@ def tiny_random(seed: int, n_max=16, m_max=4, allow_caps=True, allow_weights=Fal
     ldt = np.uint32 if dtype == "u32" else (np.float32 if dtype == "f32" else np.float64)
     return Batch(f"tiny_random_{seed}", n, m, L[None, :].astype(ldt), deg, prof,
                  caps=caps, kv_caps=kv, weights=w)
+
+
+# ----------------------------------------------------------------------------- SA randomness
+def sa_uniforms(seed: int, chains: int, iters: int, init_moves: int = 8):
+    """Pre-drawn uniforms for the simulated-annealing resource manager (Alg. 2): per chain
+    1 + 3*init_moves for the initial state and 4 per iteration (move kind, first pick, second
+    pick, acceptance).  Random numbers the method draws are inputs (R16)."""
+    rng = np.random.default_rng(SEED_BASE + 5000 + seed)
+    return rng.random((chains, 1 + 3 * init_moves)), rng.random((chains, iters, 4))

@@ -333,3 +333,25 @@ def test_bounds_checked_build():
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert "bounds violations: 0" in r.stdout, r.stdout[-2000:]
+
+
+# ------------------------------------------------------------------ N1: SA resource manager on the GPU
+def test_sa_gpu_matches_oracle_sa():
+    """Alg. 2 with batched GPU PresortedDP evaluations follows exactly the oracle's walk
+    (same pre-drawn uniforms; FP32 objectives are bit-exact, so every accept decision agrees)."""
+    from oracle import sa as osa
+    from paper_2603_28101_b200 import allocator as alloc
+    rng = np.random.default_rng(21)
+    L = wl.presort(wl.predicted(rng, wl.coding_lengths(rng, 32, 8)))          # n = 256
+    prof = wl.float_profile()
+    cfg = alloc.SAConfig(budget=48, m_min=2, m_max=40, max_iters=90)
+    iu, su = wl.sa_uniforms(3, 6, 90)
+    rm = alloc.ResourceManager(prof, n_max=256, m_max=40, chains=6)
+    res = rm.anneal(L, cfg, iu, su)
+    c, N, chains = osa.anneal(L.astype(np.float64), prof.T, prof.F, prof.degrees, 48, iu, su, m_min=2, m_max=40,
+                              max_iters=90)
+    assert res.best_makespan == c and res.best_degrees == N
+    for (cb, nb), (oc, on, otrace), gtrace in zip(res.chain_best, chains, res.trace):
+        assert cb == oc and nb == on and gtrace == otrace
+    ref = oracle.solve(oracle.Problem(L, prof.T, prof.F, prof.row_of(list(N)), mode="f32"))
+    assert np.array_equal(res.best_boundaries, ref["bounds"])
