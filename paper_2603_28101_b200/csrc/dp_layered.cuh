@@ -351,10 +351,12 @@ __global__ void __launch_bounds__(kK3Threads) k3_layer(LayerArgs la) {
     const int kend = align4(imaxb);
     const int k0 = kstart + q * kc;
     const int k1 = min(k0 + kc, kend);
-    if (a.status[b] != HEDDLE_OK) { __syncthreads(); continue; }
+    // invalid problems compute nothing but keep the block accounting of the fused exchange
+    const bool valid = a.status[b] == HEDDLE_OK;
     const L* gL = reinterpret_cast<const L*>(a.lengths) + (int64_t)b * a.ls;
     const D* gprev = reinterpret_cast<const D*>(a.dpws) + ((int64_t)b * (m + 1) + (j - 1)) * (n + 1);
     D* gcur = reinterpret_cast<D*>(a.dpws) + ((int64_t)b * (m + 1) + j) * (n + 1);
+    if (valid) {
     int row = 0;
     const int d = a.degrees[(int64_t)b * a.ds + j - 1];
     for (int qq = 0; qq < a.D; ++qq) row = (a.prof_deg[qq] == d) ? qq : row;
@@ -428,6 +430,7 @@ __global__ void __launch_bounds__(kK3Threads) k3_layer(LayerArgs la) {
         }
       }
     }
+    }   // valid
     if (la.peer_dp) {
       // last finished tile of a column block pushes the block's final row values to every peer
       // over NVLink (vector stores into the peers' dp rows), then bumps their arrival counter
@@ -478,8 +481,11 @@ struct PersistArgs {
   int64_t nentries;
   unsigned long long* counter;     // global tile counter (zeroed per solve)
   unsigned int* blk_done;          // [m+1][B][ncb] finished tiles per block (zeroed per solve)
-  unsigned long long* ready;       // [m+1][B][ncb] epoch counters of this rank
-  unsigned long long epoch;        // solves so far including this one (same on every rank)
+  unsigned long long* ready;       // [m+1][B][ncb] publication counters of this rank (zeroed per solve)
+  unsigned long long epoch;        // ready target (1: one publication per block per solve)
+  unsigned long long* const* peer_arrive;  // split mode: every rank's total-arrivals counter
+  const unsigned long long* arrive;        // this rank's total-arrivals counter (monotonic)
+  unsigned long long arrive_target;        // cumulative arrivals expected at the end of this solve
   int own_rank, own_world;
   void* const* peer_dp;            // split mode: every rank's dp workspace (null: single GPU)
   unsigned long long* const* peer_ready;   // split mode: every rank's ready array
@@ -522,9 +528,11 @@ __global__ void __launch_bounds__(kK3Threads) k5_persistent(PersistArgs pa) {
     const int kend = align4(imaxb);
     const int k0 = kstart + q * kc;
     const int k1 = min(k0 + kc, kend);
-    if (a.status[b] != HEDDLE_OK) { __syncthreads(); continue; }   // (uniform; consumers skip it too)
+    // invalid problems compute nothing but still count and publish their blocks, so that the
+    // number of arrivals every rank expects does not depend on device-side validation
+    const bool valid = a.status[b] == HEDDLE_OK;
     // ---- dependencies: row j-1 columns [max(k0, j-1), min(k1-1, n-m+j-1)] final (row 1: prologue)
-    if (j >= 3) {
+    if (valid && j >= 3) {
       if (tid == 0) {
         const int pc = (j - 1) & ~3;
         const int lo = max(k0, j - 1), hi = min(k1 - 1, n - m + j - 1);
@@ -539,6 +547,7 @@ __global__ void __launch_bounds__(kK3Threads) k5_persistent(PersistArgs pa) {
     const L* gL = reinterpret_cast<const L*>(a.lengths) + (int64_t)b * a.ls;
     const D* gprev = reinterpret_cast<const D*>(a.dpws) + ((int64_t)b * (m + 1) + (j - 1)) * (n + 1);
     D* gcur = reinterpret_cast<D*>(a.dpws) + ((int64_t)b * (m + 1) + j) * (n + 1);
+    if (valid) {
     int row = 0;
     const int d = a.degrees[(int64_t)b * a.ds + j - 1];
     for (int qq = 0; qq < a.D; ++qq) row = (a.prof_deg[qq] == d) ? qq : row;
@@ -585,6 +594,7 @@ __global__ void __launch_bounds__(kK3Threads) k5_persistent(PersistArgs pa) {
         }
       }
     }
+    }   // valid
     // ---- completion of the column block -> publish
     __threadfence();
     __syncthreads();
@@ -609,7 +619,10 @@ __global__ void __launch_bounds__(kK3Threads) k5_persistent(PersistArgs pa) {
         __syncthreads();
         if (tid == 0)
           for (int r = 0; r < pa.own_world; ++r)
-            if (r != pa.own_rank) atomicAdd_system(pa.peer_ready[r] + bidx, 1ull);
+            if (r != pa.own_rank) {
+              atomicAdd_system(pa.peer_ready[r] + bidx, 1ull);
+              atomicAdd_system(pa.peer_arrive[r], 1ull);   // total, for the end-of-solve barrier
+            }
       }
       if (tid == 0) atomicAdd_system(pa.ready + bidx, 1ull);   // local consumers
     }
@@ -617,13 +630,10 @@ __global__ void __launch_bounds__(kK3Threads) k5_persistent(PersistArgs pa) {
   }
 }
 
-// split mode: wait until the block holding column n of row m arrived for every valid problem
-__global__ void k5_wait_last(PersistArgs pa) {
-  const SolveArgs& a = pa.a;
-  const int n = a.n, m = a.m;
-  const int blk = (n - (m & ~3)) / kK3Cols;
-  for (int b = 0; b < a.B; ++b)
-    if (a.status[b] == HEDDLE_OK) wait_flag(pa.ready + ((int64_t)m * a.B + b) * pa.ncb + blk, pa.epoch, pa.err);
+// split mode: wait until every block the peers publish in this solve has arrived (all rows
+// complete for the backtrack, and no push is still in flight when the next solve resets)
+__global__ void k5_wait_arrivals(PersistArgs pa) {
+  wait_flag(pa.arrive, pa.arrive_target, pa.err);
   __threadfence();
 }
 

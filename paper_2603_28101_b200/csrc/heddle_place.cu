@@ -95,6 +95,8 @@ struct heddle_place_ctx {
   int64_t tiles_n = 0;
   int tiles_key[6] = {-1, -1, -1, -1, -1, -1};
   int64_t ready_epoch = 0;                    // solves that used d_ready (single-GPU and split)
+  unsigned long long arrive_total = 0;        // cumulative K5 arrivals expected (split mode)
+  unsigned long long** d_peer_arrive = nullptr; // device array [world]: &peer_flags[r][max_m + 1]
   std::vector<unsigned long long> expect;     // cumulative arrivals expected per counter
 };
 
@@ -321,8 +323,12 @@ heddle_status solve_persistent(heddle_place_ctx* x, SolveArgs& a, cudaStream_t s
     std::memcpy(x->tiles_key, key, sizeof(key));
   }
   x->ready_epoch++;
+  // per-solve reset (safe in split mode: peers publish into this rank only after its start
+  // signal, and the previous solve waited for all of its arrivals)
   if (cudaMemsetAsync(x->d_ctr, 0, 8, s) != cudaSuccess ||
-      cudaMemsetAsync(x->d_blkdone, 0, sizeof(unsigned) * (size_t)B * ncb * (m + 1), s) != cudaSuccess)
+      cudaMemsetAsync(x->d_blkdone, 0, sizeof(unsigned) * (size_t)B * ncb * (m + 1), s) != cudaSuccess ||
+      cudaMemsetAsync(x->d_ready, 0, 8 * (size_t)B * ncb * (m + 1), s) != cudaSuccess ||
+      cudaMemsetAsync(x->d_err, 0, sizeof(int), s) != cudaSuccess)
     return HEDDLE_E_CUDA;
   PersistArgs pa{};
   pa.a = a;
@@ -333,7 +339,7 @@ heddle_status solve_persistent(heddle_place_ctx* x, SolveArgs& a, cudaStream_t s
   pa.counter = x->d_ctr;
   pa.blk_done = x->d_blkdone;
   pa.ready = x->d_ready;
-  pa.epoch = (unsigned long long)x->ready_epoch;
+  pa.epoch = 1ull;
   pa.own_rank = rank;
   pa.own_world = world;
   pa.err = x->d_err;
@@ -347,6 +353,22 @@ heddle_status solve_persistent(heddle_place_ctx* x, SolveArgs& a, cudaStream_t s
     pa.peer_ready = x->d_peer_ready;
     pa.start_flag = x->d_flags;
     pa.wait_start = x->expect[0];
+    // arrivals: one per (problem, block of layers 2..m with computed columns) owned by another rank
+    int64_t foreign = 0;
+    for (int j = 2; j <= m; ++j) {
+      const int cbase = j & ~3, imax = n - m + j;
+      for (int blk = 0; blk < ncb; ++blk) {
+        const int c0 = cbase + kK3Cols * blk;
+        if (c0 > imax) break;
+        if (j == m && c0 + kK3Cols <= n) continue;
+        const int w = blk % (2 * world);
+        if ((w < world ? w : 2 * world - 1 - w) != rank) ++foreign;
+      }
+    }
+    x->arrive_total += (unsigned long long)foreign * B;
+    pa.peer_arrive = x->d_peer_arrive;
+    pa.arrive = x->d_flags + x->max_m + 1;
+    pa.arrive_target = x->arrive_total;
     pa.a.err = x->d_err;
     a.err = x->d_err;
   }
@@ -366,7 +388,7 @@ heddle_status solve_persistent(heddle_place_ctx* x, SolveArgs& a, cudaStream_t s
   fn<<<grid, kK3Threads, smem, s>>>(pa);
   x->launches++;
   if (world > 1) {
-    k5_wait_last<<<1, 1, 0, s>>>(pa);
+    k5_wait_arrivals<<<1, 1, 0, s>>>(pa);
     x->launches++;
   }
   if (x->trace) {
@@ -611,6 +633,7 @@ void heddle_place_destroy(heddle_place_ctx* ctx) {
   cudaFree(ctx->d_peer_dp);
   cudaFree(ctx->d_peer_flags);
   cudaFree(ctx->d_peer_ready);
+  cudaFree(ctx->d_peer_arrive);
   cudaFree(ctx->d_ready);
   cudaFree(ctx->d_tiles);
   cudaFree(ctx->d_flags);
@@ -900,8 +923,9 @@ static heddle_status setup_p2p(heddle_place_ctx* x) {
   const int world = x->split_world, rank = x->split_rank;
   DeviceGuard guard(x->device);
   const int ncb_max = (x->max_n + 3) / kK3Cols + 2;
-  if (cudaMalloc(&x->d_flags, 8 * (size_t)(x->max_m + 1)) != cudaSuccess ||
-      cudaMemset(x->d_flags, 0, 8 * (size_t)(x->max_m + 1)) != cudaSuccess ||
+  if (cudaMalloc(&x->d_flags, 8 * (size_t)(x->max_m + 2)) != cudaSuccess ||   // [max_m+1]: K5 arrivals
+      cudaMemset(x->d_flags, 0, 8 * (size_t)(x->max_m + 2)) != cudaSuccess ||
+      cudaMalloc(&x->d_peer_arrive, sizeof(void*) * world) != cudaSuccess ||
       cudaMalloc(&x->d_blkdone, sizeof(unsigned) * (size_t)x->max_batch * ncb_max * (x->max_m + 1)) != cudaSuccess ||
       cudaMalloc(&x->d_err, sizeof(int)) != cudaSuccess || cudaMemset(x->d_err, 0, sizeof(int)) != cudaSuccess ||
       cudaMalloc(&x->d_peer_dp, sizeof(void*) * world) != cudaSuccess ||
@@ -971,6 +995,11 @@ static heddle_status setup_p2p(heddle_place_ctx* x) {
   cudaMemcpy(x->d_peer_dp, x->peer_dp_h.data(), sizeof(void*) * world, cudaMemcpyHostToDevice);
   cudaMemcpy(x->d_peer_flags, x->peer_flags_h.data(), sizeof(void*) * world, cudaMemcpyHostToDevice);
   cudaMemcpy(x->d_peer_ready, x->peer_ready_h.data(), sizeof(void*) * world, cudaMemcpyHostToDevice);
+  {
+    std::vector<unsigned long long*> arr(world);
+    for (int r = 0; r < world; ++r) arr[r] = static_cast<unsigned long long*>(x->peer_flags_h[r]) + x->max_m + 1;
+    cudaMemcpy(x->d_peer_arrive, arr.data(), sizeof(void*) * world, cudaMemcpyHostToDevice);
+  }
   x->p2p = cudaGetLastError() == cudaSuccess;
   return HEDDLE_OK;
 }

@@ -355,3 +355,27 @@ def test_sa_gpu_matches_oracle_sa():
         assert cb == oc and nb == on and gtrace == otrace
     ref = oracle.solve(oracle.Problem(L, prof.T, prof.F, prof.row_of(list(N)), mode="f32"))
     assert np.array_equal(res.best_boundaries, ref["bounds"])
+
+
+@pytest.mark.parametrize("kernel", ["layered", "batched", "auto"])
+def test_context_reuse_across_shapes(kernel):
+    """One context, consecutive solves with different (B, n, m) and an invalid problem in between:
+    every solve must match the oracle (per-solve state of the persistent kernel is reset)."""
+    from paper_2603_28101_b200.placer import Placer
+    prof = wl.float_profile()
+    pl = Placer.from_profile(prof, max_n=3000, max_m=40, max_batch=5, kernel=kernel)
+    rng = np.random.default_rng(17)
+    for it, (B, n, m) in enumerate([(1, 2900, 8), (3, 1500, 37), (2, 2999, 12), (5, 700, 3), (1, 2900, 8)]):
+        L = wl.presort_rows(wl.predicted(rng, wl.coding_lengths(rng, (n * B + 7) // 8, 8)[: n * B].reshape(B, n)))
+        deg = wl.sorted_degree_vectors(rng, B, m)
+        if it == 2:
+            L[1, 5], L[1, 6] = L[1, 6], L[1, 5] + 100.0     # problem 1 unsorted
+        batch = wl.Batch("reuse", n, m, L.astype(np.float32), deg, prof)
+        g = run_gpu(batch, placer=pl)
+        for b in range(B):
+            ref = oracle.solve(oracle.Problem.from_batch(batch, b, mode="f32"))
+            if it == 2 and b == 1:
+                assert g["status"][b] == 2
+                continue
+            assert g["status"][b] == 0, (it, b, g["status"])
+            assert g["obj"][b] == ref["opt"] and np.array_equal(g["bounds"][b], ref["bounds"]), (it, b)
