@@ -119,7 +119,7 @@ __device__ __forceinline__ D shfl_down(D v, int off) { return __shfl_down_sync(0
 template <int DT> struct SpT { using type = double; };
 template <> struct SpT<HEDDLE_U32> { using type = uint64_t; };
 
-// ---- F32 min-max fast step (the paper's Eq. 3 in the default FP32 mode) -----------------
+// ---- F32 fast step (the paper's Eq. 3 in the default FP32 mode; min-plus uses FFMA2) -----
 // Two columns share one FMUL2 (mul.rn.f32x2: L[k+u] broadcast x {G[s], G[s+1]}), so a
 // cell costs 1/2 FMA-pipe issue + FMNMX(max) + 1/2 FMNMX3(min): the ALU pipe (2 cycles
 // per FMNMX / FMNMX3) is the only bound.  The pair {G[x], G[x+1]} must sit in an aligned
@@ -129,6 +129,13 @@ __device__ __forceinline__ unsigned long long f32x2_mul_bcast(float l, unsigned 
   unsigned long long l2, r;
   asm("mov.b64 %0, {%1, %1};" : "=l"(l2) : "f"(l));
   asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(l2), "l"(g2));
+  return r;
+}
+__device__ __forceinline__ unsigned long long f32x2_fma_bcast(float l, unsigned long long g2, float d) {
+  unsigned long long l2, d2, r;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(l2) : "f"(l));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(d2) : "f"(d));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(l2), "l"(g2), "l"(d2));
   return r;
 }
 __device__ __forceinline__ float min3f(float a, float b, float c) {
@@ -155,6 +162,8 @@ __device__ __forceinline__ void sweep_slide(const typename Tr<DT, SR>::L* __rest
                                             const typename Tr<DT, SR>::G* __restrict__ gcol2, int k, int iters,
                                             typename Tr<DT, SR>::D (&acc)[R], int (&arg)[R], const int (&klo)[R]) {
   using T = Tr<DT, SR>;
+  // (min-plus stays on the generic FFMA path: FFMA2 measured slower there -- its pipe, not
+  //  the ALU, becomes the bound when the combine needs no FMNMX)
   if constexpr (DT == HEDDLE_F32 && SR == HEDDLE_MINMAX && !KP && !MASKED) {
     static_assert(R % 2 == 0, "column pairs");
     constexpr int P = (R + 4) / 2;          // register pairs per window
@@ -178,11 +187,16 @@ __device__ __forceinline__ void sweep_slide(const typename Tr<DT, SR>::L* __rest
         for (int r = 0; r < R; r += 2) {
           const int x = r - u + 3;           // cells (u, r), (u, r+1) use W[x], W[x+1]
           const unsigned long long g2 = (x % 2 == 0) ? wp[x / 2] : vp[(x - 1) / 2];
-          const unsigned long long c2 = f32x2_mul_bcast(lv[u], g2);
-          float c0, c1;
-          asm("mov.b64 {%0, %1}, %2;" : "=f"(c0), "=f"(c1) : "l"(c2));
-          v[u][r] = fmaxf(dpv[u], c0);
-          v[u][r + 1] = fmaxf(dpv[u], c1);
+          if constexpr (SR == HEDDLE_MINMAX) {     // max(dp, fl(L*G)) per cell
+            const unsigned long long c2 = f32x2_mul_bcast(lv[u], g2);
+            float c0, c1;
+            asm("mov.b64 {%0, %1}, %2;" : "=f"(c0), "=f"(c1) : "l"(c2));
+            v[u][r] = fmaxf(dpv[u], c0);
+            v[u][r + 1] = fmaxf(dpv[u], c1);
+          } else {                                  // fma(L, G, dp): FFMA2, one rounding per cell
+            const unsigned long long v2 = f32x2_fma_bcast(lv[u], g2, dpv[u]);
+            asm("mov.b64 {%0, %1}, %2;" : "=f"(v[u][r]), "=f"(v[u][r + 1]) : "l"(v2));
+          }
         }
       }
 #pragma unroll

@@ -379,7 +379,11 @@ heddle_status solve_persistent(heddle_place_ctx* x, SolveArgs& a, cudaStream_t s
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kK3Threads, smem);
   if (occ < 1) return HEDDLE_E_CUDA;
   const int64_t ntiles = x->tiles_n * B;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)occ * x->num_sms));
+  // resident CTAs per SM: 3 (measured best on the large config; more CTAs stretch every tile
+  // and with it the dependency chain through the layers)
+  int per_sm = std::min(occ, 3);
+  if (const char* e = std::getenv("HEDDLE_PLACE_K5_CTAS")) per_sm = std::max(1, std::min(occ, std::atoi(e)));
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)per_sm * x->num_sms));
   std::vector<cudaEvent_t> tev(2);
   if (x->trace) {
     for (auto& e : tev) cudaEventCreate(&e);
