@@ -119,6 +119,12 @@ typedef struct {
   int64_t caps_stride;
   const int64_t* kv_caps;       /* [B][m] max group token sum, <0 = unbounded; or NULL          */
   int64_t kv_caps_stride;
+  const int32_t* weights;       /* [B][n] item weights >= 1 or NULL (= 1): an item stands for w  */
+                                /*   trajectories after short-trajectory aggregation; */
+                                /*   group size = sum of weights (R5); sum <= max_n.  Batched    */
+                                /*   (one-CTA-per-problem) kernel only: E_INVALID if n needs the  */
+                                /*   layered kernel                                             */
+  int64_t weights_stride;
 } heddle_place_problem;
 
 /* Creates a context on cfg->device: copies and validates the profile (E_RANGE

@@ -43,7 +43,8 @@ class Problem(ctypes.Structure):
                 ("lengths", ctypes.c_void_p), ("lengths_stride", ctypes.c_int64),
                 ("degrees", ctypes.c_void_p), ("degrees_stride", ctypes.c_int64),
                 ("caps", ctypes.c_void_p), ("caps_stride", ctypes.c_int64),
-                ("kv_caps", ctypes.c_void_p), ("kv_caps_stride", ctypes.c_int64)]
+                ("kv_caps", ctypes.c_void_p), ("kv_caps_stride", ctypes.c_int64),
+                ("weights", ctypes.c_void_p), ("weights_stride", ctypes.c_int64)]
 
 
 class HeddleError(RuntimeError):

@@ -16,16 +16,21 @@ constexpr int kK4Warps = 8;
 // The group cost c(k) = L[k] * G_j(cur - k) is non-increasing in k (L sorted, F non-decreasing,
 // caps only remove low k), and every candidate satisfies v(k) >= c(k) (dp >= 0), so the lowest
 // argmin lies at or after the first k in [lo, cur) with c(k) <= target: a warp-wide 32-ary search.
+// group size of items [k, cur): cur - k, or Wp[cur] - Wp[k] with aggregation weights (R5)
+__device__ __forceinline__ int gsize(const int32_t* __restrict__ gWp, int cur, int k) {
+  return gWp ? gWp[cur] - gWp[k] : cur - k;
+}
+
 template <int DT, int SR>
 __device__ int first_within_target(const typename Tr<DT, SR>::L* __restrict__ gL,
                                    const typename Tr<DT, SR>::G* __restrict__ grow, int lo, int cur,
-                                   typename Tr<DT, SR>::D target, int lane) {
+                                   typename Tr<DT, SR>::D target, int lane, const int32_t* __restrict__ gWp) {
   using T = Tr<DT, SR>;
   int a0 = lo, b0 = cur;   // first k in [a0, b0) with c(k) <= target; b0 = none
   while (b0 - a0 > 32) {
     const int step = (b0 - a0 + 31) / 32;
     const int k = a0 + lane * step;
-    const bool ok = k < b0 && T::norm(T::comb(T::zero(), gL[k], grow[cur - k])) <= target;
+    const bool ok = k < b0 && T::norm(T::comb(T::zero(), gL[k], grow[gsize(gWp, cur, k)])) <= target;
     const unsigned msk = __ballot_sync(0xffffffffu, ok);
     if (msk == 0) { a0 = min(b0, a0 + 31 * step + 1); continue; }
     const int t = __ffs(msk) - 1;
@@ -36,7 +41,7 @@ __device__ int first_within_target(const typename Tr<DT, SR>::L* __restrict__ gL
   }
   if (b0 - a0 > 0) {
     const int k = a0 + lane;
-    const bool ok = k < b0 && T::norm(T::comb(T::zero(), gL[k], grow[cur - k])) <= target;
+    const bool ok = k < b0 && T::norm(T::comb(T::zero(), gL[k], grow[gsize(gWp, cur, k)])) <= target;
     const unsigned msk = __ballot_sync(0xffffffffu, ok);
     b0 = msk ? a0 + __ffs(msk) - 1 : b0;
   }
@@ -45,11 +50,23 @@ __device__ int first_within_target(const typename Tr<DT, SR>::L* __restrict__ gL
 
 // lower split bound of layer j's group ending at cur: j-1, the size cap, the kv cap (R6)
 template <int DT, bool KV>
-__device__ int split_lower_bound(const SolveArgs& a, int b, int j, int cur, const typename SpT<DT>::type* gSp) {
+__device__ int split_lower_bound(const SolveArgs& a, int b, int j, int cur, const typename SpT<DT>::type* gSp,
+                                 const int32_t* gWp) {
   using S = typename SpT<DT>::type;
   int lo = j - 1;
   const int cap = a.caps ? a.caps[(int64_t)b * a.cs + j - 1] : -1;
-  if (cap >= 0) lo = max(lo, cur - cap);
+  if (cap >= 0) {
+    if (!gWp) {
+      lo = max(lo, cur - cap);
+    } else {   // smallest k with Wp[cur] - Wp[k] <= cap (monotone in k)
+      int l = lo, h = cur;
+      while (l < h) {
+        const int mid = (l + h) >> 1;
+        if (gWp[cur] - gWp[mid] <= cap) h = mid; else l = mid + 1;
+      }
+      lo = l;
+    }
+  }
   if constexpr (KV) {
     const int64_t kvc = a.kv[(int64_t)b * a.kvs + j - 1];
     if (kvc >= 0) {
@@ -64,7 +81,7 @@ __device__ int split_lower_bound(const SolveArgs& a, int b, int j, int cur, cons
   return lo;
 }
 
-template <int DT, int SR, bool KV>
+template <int DT, int SR, bool KV, bool W = false>
 __global__ void __launch_bounds__(32 * kK4Warps) k4_backtrack(SolveArgs a, int32_t* bounds) {
   using T = Tr<DT, SR>;
   using L = typename T::L;
@@ -84,6 +101,7 @@ __global__ void __launch_bounds__(32 * kK4Warps) k4_backtrack(SolveArgs a, int32
   const D* gdp = reinterpret_cast<const D*>(a.dpws) + (int64_t)b * (m + 1) * (n + 1);
   const G* gtab = reinterpret_cast<const G*>(a.gtab);
   const S* gSp = KV ? reinterpret_cast<const S*>(a.spws) + (int64_t)b * (n + 1) : nullptr;
+  const int32_t* gWp = W ? a.wpws + (int64_t)b * (n + 1) : nullptr;
   int cur = n;
   if (lane == 0) out[m] = n;
   for (int j = m; j >= 2; --j) {
@@ -92,13 +110,13 @@ __global__ void __launch_bounds__(32 * kK4Warps) k4_backtrack(SolveArgs a, int32
     int row = 0;
     for (int q = 0; q < a.D; ++q) row = (a.prof_deg[q] == d) ? q : row;
     const G* grow = gtab + (int64_t)row * a.gstride;
-    int lo = split_lower_bound<DT, KV>(a, b, j, cur, gSp);
-    lo = first_within_target<DT, SR>(gL, grow, lo, cur, target, lane);
+    int lo = split_lower_bound<DT, KV>(a, b, j, cur, gSp, gWp);
+    lo = first_within_target<DT, SR>(gL, grow, lo, cur, target, lane, gWp);
     int found = -1;
     for (int base = lo; base < cur && found < 0; base += 32) {
       const int k = base + lane;
       bool hit = false;
-      if (k < cur) hit = (T::norm(T::comb(gdp[(int64_t)(j - 1) * (n + 1) + k], gL[k], grow[cur - k])) == target);
+      if (k < cur) hit = (T::norm(T::comb(gdp[(int64_t)(j - 1) * (n + 1) + k], gL[k], grow[gsize(gWp, cur, k)])) == target);
       const unsigned msk = __ballot_sync(0xffffffffu, hit);
       if (msk) found = base + __ffs(msk) - 1;
     }
@@ -117,7 +135,7 @@ __global__ void __launch_bounds__(32 * kK4Warps) k4_backtrack(SolveArgs a, int32
 constexpr int kK4CtaThreads = 512;
 constexpr int kK4PerThread = 8;
 
-template <int DT, int SR, bool KV>
+template <int DT, int SR, bool KV, bool W = false>
 __global__ void __launch_bounds__(kK4CtaThreads) k4_backtrack_cta(SolveArgs a, int32_t* bounds) {
   using T = Tr<DT, SR>;
   using L = typename T::L;
@@ -137,6 +155,7 @@ __global__ void __launch_bounds__(kK4CtaThreads) k4_backtrack_cta(SolveArgs a, i
   const D* gdp = reinterpret_cast<const D*>(a.dpws) + (int64_t)b * (m + 1) * (n + 1);
   const G* gtab = reinterpret_cast<const G*>(a.gtab);
   const S* gSp = KV ? reinterpret_cast<const S*>(a.spws) + (int64_t)b * (n + 1) : nullptr;
+  const int32_t* gWp = W ? a.wpws + (int64_t)b * (n + 1) : nullptr;
   int cur = n;
   if (tid == 0) out[m] = n;
   for (int j = m; j >= 2; --j) {
@@ -146,8 +165,8 @@ __global__ void __launch_bounds__(kK4CtaThreads) k4_backtrack_cta(SolveArgs a, i
       int row = 0;
       for (int q = 0; q < a.D; ++q) row = (a.prof_deg[q] == d) ? q : row;
       const G* grow = gtab + (int64_t)row * a.gstride;
-      int lo = split_lower_bound<DT, KV>(a, b, j, cur, gSp);
-      lo = first_within_target<DT, SR>(gL, grow, lo, cur, target, lane);
+      int lo = split_lower_bound<DT, KV>(a, b, j, cur, gSp, gWp);
+      lo = first_within_target<DT, SR>(gL, grow, lo, cur, target, lane, gWp);
       if (lane == 0) { s_lo = lo; s_row = row; s_found = INT_MAX; }
     }
     __syncthreads();
@@ -158,7 +177,8 @@ __global__ void __launch_bounds__(kK4CtaThreads) k4_backtrack_cta(SolveArgs a, i
 #pragma unroll
       for (int i = 0; i < kK4PerThread; ++i) {
         const int k = base + i * kK4CtaThreads + tid;
-        if (mine == INT_MAX && k < cur && T::norm(T::comb(prev[k], gL[k], grow[cur - k])) == target) mine = k;
+        if (mine == INT_MAX && k < cur && T::norm(T::comb(prev[k], gL[k], grow[gsize(gWp, cur, k)])) == target)
+          mine = k;
       }
       mine = __reduce_min_sync(0xffffffffu, mine);
       if (lane == 0 && mine != INT_MAX) atomicMin(&s_found, mine);

@@ -56,6 +56,9 @@ struct SolveArgs {
   int64_t cs;
   const int64_t* kv;
   int64_t kvs;
+  const int32_t* w;        // [B][n] item weights (aggregation) or null
+  int64_t ws;
+  int32_t* wpws;           // [B][n+1] weight prefix sums for the backtrack (weighted mode)
   const void* gtab;        // [D][gstride] cost table, entry s = group size (1..max_n)
   int gstride;
   const int32_t* prof_deg; // [D] device copy of the profile's degrees
@@ -94,8 +97,8 @@ __device__ __forceinline__ void check_sweep(int kq, int iters, int R, int sdp_lo
 template <int DT, int SR>
 struct K2Smem {
   using T = Tr<DT, SR>;
-  int gOff, g2Off, lOff, d0Off, d1Off, kloOff, spOff, rowOff, capOff, kvOff, total;
-  __host__ __device__ K2Smem(int n, int m, bool kv) {
+  int gOff, g2Off, lOff, d0Off, d1Off, kloOff, spOff, wpOff, rowOff, capOff, kvOff, total;
+  __host__ __device__ K2Smem(int n, int m, bool kv, bool w = false) {
     int o = 0;
     auto take = [&](int bytes) { int at = o; o += (bytes + 15) & ~15; return at; };
     gOff = take((int)sizeof(typename T::G) * align4(kGPad + n + kGTail + 1));
@@ -105,6 +108,7 @@ struct K2Smem {
     d1Off = take((int)sizeof(typename T::D) * align4(n + kLPad));
     kloOff = kv ? take(4 * align4(n + kLPad)) : -1;
     spOff = kv ? take(8 * (n + 1)) : -1;
+    wpOff = w ? take(4 * align4(n + kLPad)) : -1;
     rowOff = take(4 * m);
     capOff = take(4 * m);
     kvOff = take(8 * m);
@@ -258,7 +262,47 @@ __device__ __forceinline__ void sweep_slide(const typename Tr<DT, SR>::L* __rest
   }
 }
 
-template <int DT, int SR, bool KP, bool KV>
+// Weighted items (short-trajectory aggregation; R5): the group size is
+// Wp[i] - Wp[k], so G is gathered per cell from the worker's global cost-table row (L1-resident)
+// instead of a sliding window; splits at or beyond a column give a size <= 0 (+inf).
+template <int DT, int SR, bool KP, bool MASKED, int R>
+__device__ __forceinline__ void sweep_weighted(const typename Tr<DT, SR>::L* __restrict__ sL,
+                                               const typename Tr<DT, SR>::D* __restrict__ sdp,
+                                               const int* __restrict__ sWp, const typename Tr<DT, SR>::G* __restrict__ grow,
+                                               int ghi, int c, int k, int iters, int n,
+                                               typename Tr<DT, SR>::D (&acc)[R], int (&arg)[R], const int (&klo)[R]) {
+  using T = Tr<DT, SR>;
+  int wi[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) wi[r] = sWp[max(0, min(c + r, n))];
+#pragma unroll 2
+  for (int t = 0; t < iters; ++t) {
+    typename T::D dpv[4];
+    typename T::L lv[4];
+    int wk[4];
+    ld4(sdp + k, dpv);
+    ld4(sL + k, lv);
+    ld4(sWp + k, wk);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int sz = wi[r] - wk[u];
+        const typename T::G g = (sz >= 1 && sz <= ghi) ? __ldg(grow + sz) : T::gpad();
+        typename T::D v = T::comb(dpv[u], lv[u], g);
+        if (MASKED) v = (k + u >= klo[r]) ? v : T::inf();
+        if (KP) {
+          if (v < acc[r]) { acc[r] = v; arg[r] = k + u; }
+        } else {
+          acc[r] = T::vmin(acc[r], v);
+        }
+      }
+    }
+    k += 4;
+  }
+}
+
+template <int DT, int SR, bool KP, bool KV, bool W = false>
 __global__ void __launch_bounds__(kK2Threads) k2_dp_batched(SolveArgs a) {
   using T = Tr<DT, SR>;
   using L = typename T::L;
@@ -268,7 +312,7 @@ __global__ void __launch_bounds__(kK2Threads) k2_dp_batched(SolveArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int n = a.n, m = a.m, b = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const K2Smem<DT, SR> lay(n, m, KV);
+  const K2Smem<DT, SR> lay(n, m, KV, W);
   G* sG = reinterpret_cast<G*>(smem + lay.gOff);
   G* sG2 = reinterpret_cast<G*>(smem + lay.g2Off);
   L* sL = reinterpret_cast<L*>(smem + lay.lOff);
@@ -276,6 +320,7 @@ __global__ void __launch_bounds__(kK2Threads) k2_dp_batched(SolveArgs a) {
   D* const sdp1 = reinterpret_cast<D*>(smem + lay.d1Off);
   int* sklo = KV ? reinterpret_cast<int*>(smem + lay.kloOff) : nullptr;
   S* sSp = KV ? reinterpret_cast<S*>(smem + lay.spOff) : nullptr;
+  int* sWp = W ? reinterpret_cast<int*>(smem + lay.wpOff) : nullptr;
   int* srow = reinterpret_cast<int*>(smem + lay.rowOff);
   int* scap = reinterpret_cast<int*>(smem + lay.capOff);
   int64_t* skv = reinterpret_cast<int64_t*>(smem + lay.kvOff);
@@ -312,6 +357,21 @@ __global__ void __launch_bounds__(kK2Threads) k2_dp_batched(SolveArgs a) {
     scap[j] = a.caps ? a.caps[(int64_t)b * a.cs + j] : -1;
     skv[j] = KV ? a.kv[(int64_t)b * a.kvs + j] : -1;
   }
+  if constexpr (W) {   // weight prefix sums Wp (R5): exact, left to right; sizes must fit the cost table
+    if (tid == 0) {
+      int acc = 0;
+      sWp[0] = 0;
+      bool ok = true;
+      for (int t = 0; t < n; ++t) {
+        const int wt = a.w[(int64_t)b * a.ws + t];
+        ok = ok && wt >= 1 && acc <= a.gstride - 1 - wt;
+        acc += wt > 0 ? wt : 0;
+        sWp[t + 1] = acc;
+      }
+      if (!ok) atomicMin(&s_err, (int)HEDDLE_E_RANGE);
+    }
+    for (int t = n + 1 + tid; t < align4(n + kLPad); t += kK2Threads) sWp[t] = INT_MAX / 2;   // beyond n: size < 0
+  }
   __syncthreads();
   int err = s_err == INT_MAX ? 0 : s_err;
   if (err == 0 && n < m) err = HEDDLE_E_INFEASIBLE;
@@ -336,6 +396,10 @@ __global__ void __launch_bounds__(kK2Threads) k2_dp_batched(SolveArgs a) {
     S* gSp = reinterpret_cast<S*>(a.spws) + (int64_t)b * (n + 1);   // for the backtrack
     for (int t = tid; t <= n; t += kK2Threads) gSp[t] = sSp[t];
   }
+  if constexpr (W) {
+    int32_t* gWp = a.wpws + (int64_t)b * (n + 1);   // for the backtrack
+    for (int t = tid; t <= n; t += kK2Threads) gWp[t] = sWp[t];
+  }
   for (int t = tid; t < align4(n + kLPad); t += kK2Threads) { sdp0[t] = T::inf(); sdp1[t] = T::inf(); }
 
   // ---------------- layers
@@ -346,7 +410,9 @@ __global__ void __launch_bounds__(kK2Threads) k2_dp_batched(SolveArgs a) {
     // cost table of worker j: G_j[s] for s = 1..min(n, cap), +inf padding elsewhere
     // (rebuilt only when the worker's profile row or cap changes: sorted degree
     //  vectors over a few MP degrees change row at most D-1 times per problem)
-    if (j == 1 || srow[j - 1] != srow[j - 2] || scap[j - 1] != scap[j - 2]) {
+    const G* const growj = gtab + (int64_t)srow[j - 1] * a.gstride;   // weighted mode: gathered per cell
+    const int ghi = (scap[j - 1] >= 0 && scap[j - 1] < a.gstride - 1) ? scap[j - 1] : a.gstride - 1;
+    if (!W && (j == 1 || srow[j - 1] != srow[j - 2] || scap[j - 1] != scap[j - 2])) {
       const G* grow = gtab + (int64_t)srow[j - 1] * a.gstride;
       const int cap = scap[j - 1];
       const int hi = (cap >= 0 && cap < n) ? cap : n;
@@ -388,7 +454,10 @@ __global__ void __launch_bounds__(kK2Threads) k2_dp_batched(SolveArgs a) {
     if (j == 1) {
       // dp[1][i] = L(tau_1) * T * F(i), i in [1, n-m+1]
       for (int i = 1 + tid; i <= imax_layer; i += kK2Threads) {
-        D v = T::comb(T::zero(), sL[0], sG[kGPad + i]);
+        G g1;
+        if constexpr (W) g1 = (sWp[i] <= ghi) ? growj[sWp[i]] : T::gpad();
+        else g1 = sG[kGPad + i];
+        D v = T::comb(T::zero(), sL[0], g1);
         if constexpr (KV) { if (sklo[i] > 0) v = T::inf(); }
         v = T::norm(v);
         cur[i] = v;
@@ -401,7 +470,10 @@ __global__ void __launch_bounds__(kK2Threads) k2_dp_batched(SolveArgs a) {
       D best = T::inf();
       int bk = INT_MAX;
       for (int k = max(m - 1, klo0) + tid; k < n; k += kK2Threads) {
-        D v = T::comb(prev[k], sL[k], sG[kGPad + n - k]);
+        G gk;
+        if constexpr (W) gk = (sWp[n] - sWp[k] <= ghi) ? growj[sWp[n] - sWp[k]] : T::gpad();
+        else gk = sG[kGPad + n - k];
+        D v = T::comb(prev[k], sL[k], gk);
         if (v < best) { best = v; bk = k; }
       }
 #pragma unroll
@@ -446,10 +518,16 @@ __global__ void __launch_bounds__(kK2Threads) k2_dp_batched(SolveArgs a) {
 #pragma unroll
           for (int r = 0; r < kLaneCols; ++r) klo[r] = sklo[min(max(c + r, j), imax)];
         }
-        check_sweep(kstart + kg * Q, Q / 4, kLaneCols, 0, align4(n + kLPad), 0, align4(kGPad + n + kGTail + 1),
-                    kGPad + c);
-        sweep_slide<DT, SR, KP, KV, kLaneCols>(sL, prev, sG + kGPad + c, sG2 + kGPad + c, kstart + kg * Q, Q / 4,
-                                               acc, arg, klo);
+        if constexpr (W) {
+          HP_CHECK(kstart + kg * Q >= 0 && kstart + kg * Q + Q + 3 < align4(n + kLPad));
+          sweep_weighted<DT, SR, KP, KV, kLaneCols>(sL, prev, sWp, growj, ghi, c, kstart + kg * Q, Q / 4, n, acc,
+                                                    arg, klo);
+        } else {
+          check_sweep(kstart + kg * Q, Q / 4, kLaneCols, 0, align4(n + kLPad), 0, align4(kGPad + n + kGTail + 1),
+                      kGPad + c);
+          sweep_slide<DT, SR, KP, KV, kLaneCols>(sL, prev, sG + kGPad + c, sG2 + kGPad + c, kstart + kg * Q, Q / 4,
+                                                 acc, arg, klo);
+        }
         // combine the kSplitLanes partial minima of each column (lowest split on ties)
 #pragma unroll
         for (int off = kColLanes; off < 32; off <<= 1) {

@@ -65,6 +65,8 @@ struct heddle_place_ctx {
   int k2_smem_max = 0;
   int num_sms = 0;
   int32_t* d_klo = nullptr;             // [max_batch][max_n+1] (layered kernel, kv caps)
+  int32_t* d_wp = nullptr;              // [max_batch][max_n+1] weight prefix sums (weighted problems)
+  bool last_w = false;
   unsigned long long* d_keys = nullptr; // [max_batch][max_n+1] (layered kernel, KEEP_PARENTS)
   unsigned long long* d_ctr = nullptr;  // [max_m+1] dynamic tile counters of the layered kernel
   bool last_layered = false;
@@ -123,28 +125,34 @@ using K2Fn = void (*)(SolveArgs);
 using K4Fn = void (*)(SolveArgs, int32_t*);
 
 template <int DT, int SR>
-K2Fn pick_k2(bool kp, bool kv) {
+K2Fn pick_k2(bool kp, bool kv, bool w) {
+  if (w) {
+    if (kp) return kv ? k2_dp_batched<DT, SR, true, true, true> : k2_dp_batched<DT, SR, true, false, true>;
+    return kv ? k2_dp_batched<DT, SR, false, true, true> : k2_dp_batched<DT, SR, false, false, true>;
+  }
   if (kp) return kv ? k2_dp_batched<DT, SR, true, true> : k2_dp_batched<DT, SR, true, false>;
   return kv ? k2_dp_batched<DT, SR, false, true> : k2_dp_batched<DT, SR, false, false>;
 }
 template <int DT, int SR>
-K4Fn pick_k4(bool kv) {
+K4Fn pick_k4(bool kv, bool w) {
+  if (w) return kv ? k4_backtrack<DT, SR, true, true> : k4_backtrack<DT, SR, false, true>;
   return kv ? k4_backtrack<DT, SR, true> : k4_backtrack<DT, SR, false>;
 }
 template <int DT, int SR>
-K4Fn pick_k4c(bool kv) {
+K4Fn pick_k4c(bool kv, bool w) {
+  if (w) return kv ? k4_backtrack_cta<DT, SR, true, true> : k4_backtrack_cta<DT, SR, false, true>;
   return kv ? k4_backtrack_cta<DT, SR, true> : k4_backtrack_cta<DT, SR, false>;
 }
 
-K2Fn k2_for(int dt, int sr, bool kp, bool kv) {
-  if (dt == HEDDLE_F32) return sr == HEDDLE_MINMAX ? pick_k2<HEDDLE_F32, HEDDLE_MINMAX>(kp, kv) : pick_k2<HEDDLE_F32, HEDDLE_MINPLUS>(kp, kv);
-  if (dt == HEDDLE_F64) return sr == HEDDLE_MINMAX ? pick_k2<HEDDLE_F64, HEDDLE_MINMAX>(kp, kv) : pick_k2<HEDDLE_F64, HEDDLE_MINPLUS>(kp, kv);
-  return sr == HEDDLE_MINMAX ? pick_k2<HEDDLE_U32, HEDDLE_MINMAX>(kp, kv) : pick_k2<HEDDLE_U32, HEDDLE_MINPLUS>(kp, kv);
+K2Fn k2_for(int dt, int sr, bool kp, bool kv, bool w = false) {
+  if (dt == HEDDLE_F32) return sr == HEDDLE_MINMAX ? pick_k2<HEDDLE_F32, HEDDLE_MINMAX>(kp, kv, w) : pick_k2<HEDDLE_F32, HEDDLE_MINPLUS>(kp, kv, w);
+  if (dt == HEDDLE_F64) return sr == HEDDLE_MINMAX ? pick_k2<HEDDLE_F64, HEDDLE_MINMAX>(kp, kv, w) : pick_k2<HEDDLE_F64, HEDDLE_MINPLUS>(kp, kv, w);
+  return sr == HEDDLE_MINMAX ? pick_k2<HEDDLE_U32, HEDDLE_MINMAX>(kp, kv, w) : pick_k2<HEDDLE_U32, HEDDLE_MINPLUS>(kp, kv, w);
 }
-K4Fn k4_for(int dt, int sr, bool kv) {
-  if (dt == HEDDLE_F32) return sr == HEDDLE_MINMAX ? pick_k4<HEDDLE_F32, HEDDLE_MINMAX>(kv) : pick_k4<HEDDLE_F32, HEDDLE_MINPLUS>(kv);
-  if (dt == HEDDLE_F64) return sr == HEDDLE_MINMAX ? pick_k4<HEDDLE_F64, HEDDLE_MINMAX>(kv) : pick_k4<HEDDLE_F64, HEDDLE_MINPLUS>(kv);
-  return sr == HEDDLE_MINMAX ? pick_k4<HEDDLE_U32, HEDDLE_MINMAX>(kv) : pick_k4<HEDDLE_U32, HEDDLE_MINPLUS>(kv);
+K4Fn k4_for(int dt, int sr, bool kv, bool w) {
+  if (dt == HEDDLE_F32) return sr == HEDDLE_MINMAX ? pick_k4<HEDDLE_F32, HEDDLE_MINMAX>(kv, w) : pick_k4<HEDDLE_F32, HEDDLE_MINPLUS>(kv, w);
+  if (dt == HEDDLE_F64) return sr == HEDDLE_MINMAX ? pick_k4<HEDDLE_F64, HEDDLE_MINMAX>(kv, w) : pick_k4<HEDDLE_F64, HEDDLE_MINPLUS>(kv, w);
+  return sr == HEDDLE_MINMAX ? pick_k4<HEDDLE_U32, HEDDLE_MINMAX>(kv, w) : pick_k4<HEDDLE_U32, HEDDLE_MINPLUS>(kv, w);
 }
 
 using K3Fn = void (*)(LayerArgs);
@@ -168,15 +176,15 @@ KPro pick_pro(bool kp, bool kv) {
                       : (sr == HEDDLE_MINMAX ? NAME<HEDDLE_U32, HEDDLE_MINMAX>(__VA_ARGS__)             \
                                              : NAME<HEDDLE_U32, HEDDLE_MINPLUS>(__VA_ARGS__)))
 K3Fn k3_for(int dt, int sr, bool kp, bool kv) { return HP_DISPATCH(pick_k3, kp, kv); }
-K4Fn k4c_for(int dt, int sr, bool kv) { return HP_DISPATCH(pick_k4c, kv); }
+K4Fn k4c_for(int dt, int sr, bool kv, bool w) { return HP_DISPATCH(pick_k4c, kv, w); }
 KPro pro_for(int dt, int sr, bool kp, bool kv) { return HP_DISPATCH(pick_pro, kp, kv); }
 template <int DT, int SR> int k3_smem_t(int kc) { return K3Smem<DT, SR>(kc).total; }
 int k3_smem(int dt, int sr, int kc) { return HP_DISPATCH(k3_smem_t, kc); }
 
-int k2_smem(int dt, int sr, int n, int m, bool kv) {
-  if (dt == HEDDLE_F32) return sr == HEDDLE_MINMAX ? K2Smem<HEDDLE_F32, HEDDLE_MINMAX>(n, m, kv).total : K2Smem<HEDDLE_F32, HEDDLE_MINPLUS>(n, m, kv).total;
-  if (dt == HEDDLE_F64) return sr == HEDDLE_MINMAX ? K2Smem<HEDDLE_F64, HEDDLE_MINMAX>(n, m, kv).total : K2Smem<HEDDLE_F64, HEDDLE_MINPLUS>(n, m, kv).total;
-  return sr == HEDDLE_MINMAX ? K2Smem<HEDDLE_U32, HEDDLE_MINMAX>(n, m, kv).total : K2Smem<HEDDLE_U32, HEDDLE_MINPLUS>(n, m, kv).total;
+int k2_smem(int dt, int sr, int n, int m, bool kv, bool w = false) {
+  if (dt == HEDDLE_F32) return sr == HEDDLE_MINMAX ? K2Smem<HEDDLE_F32, HEDDLE_MINMAX>(n, m, kv, w).total : K2Smem<HEDDLE_F32, HEDDLE_MINPLUS>(n, m, kv, w).total;
+  if (dt == HEDDLE_F64) return sr == HEDDLE_MINMAX ? K2Smem<HEDDLE_F64, HEDDLE_MINMAX>(n, m, kv, w).total : K2Smem<HEDDLE_F64, HEDDLE_MINPLUS>(n, m, kv, w).total;
+  return sr == HEDDLE_MINMAX ? K2Smem<HEDDLE_U32, HEDDLE_MINMAX>(n, m, kv, w).total : K2Smem<HEDDLE_U32, HEDDLE_MINPLUS>(n, m, kv, w).total;
 }
 
 template <int DT, int SR>
@@ -624,6 +632,7 @@ void heddle_place_destroy(heddle_place_ctx* ctx) {
   cudaFree(ctx->d_status);
   cudaFree(ctx->d_stage);
   cudaFree(ctx->d_klo);
+  cudaFree(ctx->d_wp);
   cudaFree(ctx->d_keys);
   cudaFree(ctx->d_ctr);
   cudaFree(ctx->d_send);
@@ -744,8 +753,8 @@ heddle_status heddle_place_init(const heddle_place_config* c, heddle_place_ctx**
   // opt in to large dynamic shared memory for every K2 variant this ctx may launch
   // (the dynamic limit is the opt-in maximum minus the kernel's static shared memory)
   for (int kp = 0; kp < 2; ++kp)
-    for (int kv = 0; kv < 2; ++kv) {
-      const void* fn = reinterpret_cast<const void*>(k2_for(x->dtype, x->semiring, kp, kv));
+    for (int kv = 0; kv < 4; ++kv) {
+      const void* fn = reinterpret_cast<const void*>(k2_for(x->dtype, x->semiring, kp, kv & 1, kv >> 1));
       cudaFuncAttributes fa{};
       if (cudaFuncGetAttributes(&fa, fn) != cudaSuccess ||
           cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -768,12 +777,14 @@ heddle_status heddle_place_solve(heddle_place_ctx* x, const heddle_place_problem
     return HEDDLE_E_INVALID;
   const bool kv = p->kv_caps != nullptr;
   const bool kp = (x->flags & HEDDLE_KEEP_PARENTS) != 0;
-  const int smem2 = k2_smem(x->dtype, x->semiring, p->n, p->m, kv);
+  const bool wt = p->weights != nullptr;
+  if (wt && p->weights_stride < 0) return HEDDLE_E_INVALID;
+  const int smem2 = k2_smem(x->dtype, x->semiring, p->n, p->m, kv, wt);
   const bool k2_fits = smem2 <= x->k2_smem_max;
   const bool wide = (x->dtype == HEDDLE_F64) || (x->dtype == HEDDLE_U32 && x->semiring == HEDDLE_MINPLUS);
   bool layered;
   if (x->split_world > 1) layered = true;
-  else if (x->flags & HEDDLE_FORCE_BATCHED) layered = false;
+  else if (wt || (x->flags & HEDDLE_FORCE_BATCHED)) layered = false;   // weights: batched kernel only
   else if (x->flags & HEDDLE_FORCE_LAYERED) layered = true;
   else layered = !k2_fits || use_layered(x, p->n, p->m, p->B);
   if (!layered && !k2_fits) return HEDDLE_E_INVALID;   // n too large for the one-CTA-per-problem kernel
@@ -792,6 +803,12 @@ heddle_status heddle_place_solve(heddle_place_ctx* x, const heddle_place_problem
   a.cs = p->caps_stride;
   a.kv = p->kv_caps;
   a.kvs = p->kv_caps_stride;
+  a.w = p->weights;
+  a.ws = p->weights_stride;
+  if (wt && !x->d_wp) {
+    if (cudaMalloc(&x->d_wp, 4 * (size_t)x->max_batch * (x->max_n + 1)) != cudaSuccess) { cudaGetLastError(); return HEDDLE_E_NOMEM; }
+  }
+  a.wpws = x->d_wp;
   a.gtab = x->d_gtab;
   a.gstride = x->gstride;
   a.prof_deg = x->d_prof_deg;
@@ -805,7 +822,7 @@ heddle_status heddle_place_solve(heddle_place_ctx* x, const heddle_place_problem
   a.objective = objective_out;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (!layered) {
-    k2_for(x->dtype, x->semiring, kp, kv)<<<p->B, kK2Threads, smem2, s>>>(a);
+    k2_for(x->dtype, x->semiring, kp, kv, wt)<<<p->B, kK2Threads, smem2, s>>>(a);
     x->launches++;
     if (cudaGetLastError() != cudaSuccess) return HEDDLE_E_CUDA;
   } else {
@@ -814,6 +831,7 @@ heddle_status heddle_place_solve(heddle_place_ctx* x, const heddle_place_problem
   }
   x->last = a;
   x->last_kv = kv;
+  x->last_w = wt;
   x->last_layered = layered;
   x->solved = true;
   return HEDDLE_OK;
@@ -830,9 +848,10 @@ heddle_status heddle_place_backtrack(heddle_place_ctx* x, int32_t* boundaries_ou
   // few min-plus problems: a CTA per problem (the cost bound prunes little there, so the
   // lowest-argmin scan can cover tens of thousands of splits per layer at large n)
   if (a.B < x->num_sms && x->semiring == HEDDLE_MINPLUS)
-    k4c_for(x->dtype, x->semiring, x->last_kv)<<<a.B, kK4CtaThreads, 0, s>>>(a, boundaries_out);
+    k4c_for(x->dtype, x->semiring, x->last_kv, x->last_w)<<<a.B, kK4CtaThreads, 0, s>>>(a, boundaries_out);
   else
-    k4_for(x->dtype, x->semiring, x->last_kv)<<<(a.B + kK4Warps - 1) / kK4Warps, 32 * kK4Warps, 0, s>>>(a, boundaries_out);
+    k4_for(x->dtype, x->semiring, x->last_kv, x->last_w)<<<(a.B + kK4Warps - 1) / kK4Warps, 32 * kK4Warps, 0, s>>>(
+        a, boundaries_out);
   x->launches++;
   if (cudaGetLastError() != cudaSuccess) return HEDDLE_E_CUDA;
   if (parents_out) {
@@ -860,10 +879,12 @@ heddle_status heddle_place_solve_host(heddle_place_ctx* x, const heddle_place_pr
   const int64_t drows = p.degrees_stride == 0 ? 1 : B;
   const int64_t crows = p.caps ? (p.caps_stride == 0 ? 1 : B) : 0;
   const int64_t krows = p.kv_caps ? (p.kv_caps_stride == 0 ? 1 : B) : 0;
+  const int64_t wrows = p.weights ? (p.weights_stride == 0 ? 1 : B) : 0;
   auto al = [](size_t v) { return (v + 255) & ~(size_t)255; };
   const size_t bl = al(es * lrows * n), bd = al(4 * drows * m), bc = al(4 * crows * m), bk = al(8 * krows * m);
+  const size_t bw = al(4 * wrows * n);
   const size_t bo = al(8 * B), bb = al(4 * B * (m + 1)), bs = al(4 * B);
-  const size_t need = bl + bd + bc + bk + bo + bb + bs;
+  const size_t need = bl + bd + bc + bk + bo + bb + bs + bw;
   if (need > x->stage_bytes) {
     cudaFree(x->d_stage);
     x->d_stage = nullptr;
@@ -873,6 +894,7 @@ heddle_status heddle_place_solve_host(heddle_place_ctx* x, const heddle_place_pr
   }
   char* base = static_cast<char*>(x->d_stage);
   char *dl = base, *dd = dl + bl, *dc = dd + bd, *dk = dc + bc, *dob = dk + bk, *dbd = dob + bo, *dst = dbd + bb;
+  char* dw = dst + bs;
   int64_t h2d = 0, d2h = 0;
   auto up = [&](void* dst_, const void* src, int64_t rows, int64_t cols, int64_t stride, size_t esz) -> bool {
     if (rows == 0) return true;
@@ -883,7 +905,8 @@ heddle_status heddle_place_solve_host(heddle_place_ctx* x, const heddle_place_pr
     return cudaMemcpy2DAsync(dst_, w, src, esz * stride, w, rows, cudaMemcpyHostToDevice, s) == cudaSuccess;
   };
   if (!up(dl, p.lengths, lrows, n, p.lengths_stride, es) || !up(dd, p.degrees, drows, m, p.degrees_stride, 4) ||
-      !up(dc, p.caps, crows, m, p.caps_stride, 4) || !up(dk, p.kv_caps, krows, m, p.kv_caps_stride, 8))
+      !up(dc, p.caps, crows, m, p.caps_stride, 4) || !up(dk, p.kv_caps, krows, m, p.kv_caps_stride, 8) ||
+      !up(dw, p.weights, wrows, n, p.weights_stride, 4))
     return HEDDLE_E_CUDA;
   heddle_place_problem q = p;
   q.lengths = dl;
@@ -894,6 +917,8 @@ heddle_status heddle_place_solve_host(heddle_place_ctx* x, const heddle_place_pr
   q.caps_stride = p.caps_stride == 0 ? 0 : m;
   q.kv_caps = p.kv_caps ? reinterpret_cast<const int64_t*>(dk) : nullptr;
   q.kv_caps_stride = p.kv_caps_stride == 0 ? 0 : m;
+  q.weights = p.weights ? reinterpret_cast<const int32_t*>(dw) : nullptr;
+  q.weights_stride = p.weights_stride == 0 ? 0 : n;
   heddle_status st = heddle_place_solve(x, &q, dob, reinterpret_cast<int32_t*>(dst), stream);
   if (st != HEDDLE_OK) return st;
   st = heddle_place_backtrack(x, reinterpret_cast<int32_t*>(dbd), nullptr, stream);

@@ -126,6 +126,11 @@ __device__ __forceinline__ void ld4<uint32_t>(const uint32_t* p, uint32_t (&o)[4
   o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
 }
 template <>
+__device__ __forceinline__ void ld4<int>(const int* p, int (&o)[4]) {
+  int4 v = *reinterpret_cast<const int4*>(p);
+  o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+}
+template <>
 __device__ __forceinline__ void ld4<double>(const double* p, double (&o)[4]) {
   double2 a = reinterpret_cast<const double2*>(p)[0];
   double2 b = reinterpret_cast<const double2*>(p)[1];

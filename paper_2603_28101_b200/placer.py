@@ -101,7 +101,7 @@ class Placer:
     def launches(self) -> int:
         return int(C.lib().heddle_place_launch_count(self._h))
 
-    def _problem(self, lengths, degrees, caps, kv_caps):
+    def _problem(self, lengths, degrees, caps, kv_caps, weights=None):
         if lengths.dim() == 1:
             lengths = lengths[None, :]
         B, n = lengths.shape
@@ -111,22 +111,25 @@ class Placer:
             m = degrees.shape[-1]
         if lengths.dtype != _TORCH_DT[self.dtype]:
             raise TypeError(f"lengths must be {_TORCH_DT[self.dtype]}, got {lengths.dtype}")
-        for t, nm in ((lengths, "lengths"), (degrees, "degrees"), (caps, "caps"), (kv_caps, "kv_caps")):
+        for t, nm in ((lengths, "lengths"), (degrees, "degrees"), (caps, "caps"), (kv_caps, "kv_caps"),
+                      (weights, "weights")):
             if t is not None and t.device != self.device:
                 raise ValueError(f"{nm} must live on {self.device}")
         L, ls = _rows(lengths, B, n, "lengths")
         D, ds = _rows(degrees.to(torch.int32), B, m, "degrees")
         Cp, cs = _rows(None if caps is None else caps.to(torch.int32), B, m, "caps")
         K, ks = _rows(None if kv_caps is None else kv_caps.to(torch.int64), B, m, "kv_caps")
-        keep = (L, D, Cp, K)
+        Wt, wts = _rows(None if weights is None else weights.to(torch.int32), B, n, "weights")
+        keep = (L, D, Cp, K, Wt)
         p = C.Problem(n, m, B, L.data_ptr(), ls, D.data_ptr(), ds, Cp.data_ptr() if Cp is not None else None, cs,
-                      K.data_ptr() if K is not None else None, ks)
+                      K.data_ptr() if K is not None else None, ks, Wt.data_ptr() if Wt is not None else None, wts)
         return p, keep, B, n, m
 
-    def solve(self, lengths, degrees, caps=None, kv_caps=None, stream=None):
+    def solve(self, lengths, degrees, caps=None, kv_caps=None, stream=None, weights=None):
         """Enqueue the DP on `stream` (default: torch's current stream).  Returns
-        (objective[B], status[B]) device tensors."""
-        p, keep, B, n, m = self._problem(lengths, degrees, caps, kv_caps)
+        (objective[B], status[B]) device tensors.  `weights` ([B, n] int >= 1): aggregated items
+        (short-trajectory aggregation); group size = sum of weights."""
+        p, keep, B, n, m = self._problem(lengths, degrees, caps, kv_caps, weights)
         obj = torch.empty(B, dtype=self.objective_dtype, device=self.device)
         st = torch.empty(B, dtype=torch.int32, device=self.device)
         s = (stream or torch.cuda.current_stream(self.device)).cuda_stream
@@ -147,7 +150,7 @@ class Placer:
                 "heddle_place_backtrack")
         return (bnd, par) if parents else bnd
 
-    def solve_host(self, lengths, degrees, caps=None, kv_caps=None, stream=None):
+    def solve_host(self, lengths, degrees, caps=None, kv_caps=None, stream=None, weights=None):
         """End to end with host (numpy / pinned torch CPU) buffers: H2D, solve, backtrack, D2H.
         Returns (objective, boundaries, status, bytes_h2d, bytes_d2h) as host arrays."""
         def host(a, dt):
@@ -162,14 +165,16 @@ class Placer:
         Dh = host(degrees, torch.int32)
         Ch = host(caps, torch.int32)
         Kh = host(kv_caps, torch.int64)
+        Wh = host(weights, torch.int32)
         B, n = Lh.shape
         m = Dh.shape[-1]
         L, ls = _rows(Lh, B, n, "lengths")
         D, ds = _rows(Dh, B, m, "degrees")
         Cp, cs = _rows(Ch, B, m, "caps")
         K, ks = _rows(Kh, B, m, "kv_caps")
+        Wt, wts = _rows(Wh, B, n, "weights")
         p = C.Problem(n, m, B, L.data_ptr(), ls, D.data_ptr(), ds, Cp.data_ptr() if Cp is not None else None, cs,
-                      K.data_ptr() if K is not None else None, ks)
+                      K.data_ptr() if K is not None else None, ks, Wt.data_ptr() if Wt is not None else None, wts)
         obj = torch.empty(B, dtype=self.objective_dtype).pin_memory()
         bnd = torch.empty((B, m + 1), dtype=torch.int32).pin_memory()
         st = torch.empty(B, dtype=torch.int32).pin_memory()

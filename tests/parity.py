@@ -31,8 +31,10 @@ def run_gpu(batch, semiring="minmax", keep_parents=False, dtype=None, placer=Non
             kernel="auto"):
     dtype = dtype or batch.profile.dtype
     if placer is None:
+        # weighted items: group sizes reach the total weight, which must fit the cost table (max_n)
+        max_n = batch.n if batch.weights is None else max(batch.n, int(batch.weights.sum(axis=1).max()))
         placer = Placer(batch.profile.degrees, batch.profile.T, batch.profile.F, dtype=dtype, semiring=semiring,
-                        max_n=batch.n, max_m=batch.m, max_batch=batch.B, keep_parents=keep_parents, kernel=kernel)
+                        max_n=max_n, max_m=batch.m, max_batch=batch.B, keep_parents=keep_parents, kernel=kernel)
     L = to_dev(batch.lengths[:1] if lengths_shared else batch.lengths, TDT[dtype])
     if lengths_shared:
         L = L[0]
@@ -40,7 +42,8 @@ def run_gpu(batch, semiring="minmax", keep_parents=False, dtype=None, placer=Non
     D = to_dev(batch.degrees.astype(np.int32))
     caps = None if batch.caps is None else to_dev(batch.caps.astype(np.int32))
     kv = None if batch.kv_caps is None else to_dev(batch.kv_caps.astype(np.int64))
-    obj, st = placer.solve(L, D, caps=caps, kv_caps=kv)
+    w = None if batch.weights is None else to_dev(batch.weights.astype(np.int32))
+    obj, st = placer.solve(L, D, caps=caps, kv_caps=kv, weights=w)
     if keep_parents:
         bnd, par = placer.backtrack(parents=True)
     else:

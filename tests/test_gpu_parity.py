@@ -379,3 +379,43 @@ def test_context_reuse_across_shapes(kernel):
                 continue
             assert g["status"][b] == 0, (it, b, g["status"])
             assert g["obj"][b] == ref["opt"] and np.array_equal(g["bounds"][b], ref["bounds"]), (it, b)
+
+
+# ------------------------------------------------------------------ N2: weighted items (aggregation)
+@pytest.mark.parametrize("semiring", ["minmax", "minplus"])
+@pytest.mark.parametrize("dtype", ["u32", "f32"])
+def test_weighted_random_tiny_exact(dtype, semiring):
+    """Item weights (group size = sum of weights, R5) with caps / kv caps / ties: bit-exact."""
+    sr = oracle.MINMAX if semiring == "minmax" else oracle.MINPLUS
+    done = 0
+    for s in range(200):
+        batch = wl.tiny_random(s, n_max=20, m_max=6, allow_caps=True, allow_kv=True, allow_weights=True,
+                               dtype=dtype)
+        if batch.weights is None:
+            continue
+        done += 1
+        kp = s % 2 == 0
+        gpu = run_gpu(batch, semiring=semiring, keep_parents=kp)
+        ref = oracle.solve(oracle.Problem.from_batch(batch, 0, mode=dtype, semiring=sr), want_tables=True)
+        assert_exact(gpu, 0, ref, batch, dtype, semiring, check_parents=kp, tag=f"w{dtype}{s}")
+        gpu["placer"].close()
+    assert done > 50
+
+
+def test_aggregated_rollout_matches_weighted_oracle():
+    """The paper's aggregation heuristic on the rollout workload: aggregate, weighted GPU solve,
+    expand; equal to the oracle's weighted DP and never better than the exact optimum."""
+    from paper_2603_28101_b200.aggregate import aggregate_short, expand_boundaries
+    for prob in range(3):
+        b = wl.config_rollout(problem=prob)
+        L = b.lengths[0]
+        agg, w, st = aggregate_short(L, float(np.percentile(L, 70)), 8)
+        ab = wl.Batch("agg", agg.size, b.m, agg[None, :].astype(np.float32), b.degrees, b.profile,
+                      weights=w[None, :])
+        g = run_gpu(ab, keep_parents=True)
+        ref = oracle.solve(oracle.Problem.from_batch(ab, 0, mode="f32"), want_tables=True)
+        assert_exact(g, 0, ref, ab, "f32", "minmax", check_parents=True, tag=f"agg{prob}")
+        exact = oracle.solve(oracle.Problem.from_batch(b, 0, mode="f32"))
+        assert g["obj"][0] >= exact["opt"]
+        full = expand_boundaries(g["bounds"][0], st)
+        assert full[0] == 0 and full[-1] == b.n and np.all(np.diff(full) > 0)
