@@ -190,6 +190,17 @@ heddle_status heddle_place_init_split(const heddle_place_config* cfg, const void
                                       int32_t world, heddle_place_ctx** out);
 int32_t heddle_place_split_blocks(int32_t ncb, int32_t world, int32_t rank, int32_t* blocks_out, int32_t cap);
 
+/* Migration retarget (§5.3).  For each query q: problem
+ * query_problem[q] with plan boundaries[b][0..m] (from heddle_place_backtrack; n = b_m), n_active[b]
+ * remaining active trajectories n*, and the trajectory's 0-based rank among them by updated
+ * predicted length (descending) -> worker_out[q] = the group whose range covers the rank under
+ * capacities ceil(s_i * n* / n), s_i = b_{i+1} - b_i (ranks past the scaled total: worker m-1);
+ * -1 for an invalid query (bad problem index, rank outside [0, n*), n* < 1).  All pointers are
+ * device memory; asynchronous on `stream`; needs no context. */
+heddle_status heddle_place_retarget(const int32_t* boundaries, int32_t m, int32_t B, const int32_t* n_active,
+                                    const int32_t* query_problem, const int32_t* query_rank, int32_t nq,
+                                    int32_t* worker_out, void* stream);
+
 /* Debug builds only (compiled with -DHEDDLE_CHECK_BOUNDS): number of shared-memory index-range
  * violations the kernels detected so far on the current device; -1 in release builds. */
 int64_t heddle_place_debug_violations(void);

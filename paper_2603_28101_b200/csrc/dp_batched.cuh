@@ -303,7 +303,10 @@ __device__ __forceinline__ void sweep_weighted(const typename Tr<DT, SR>::L* __r
 }
 
 template <int DT, int SR, bool KP, bool KV, bool W = false>
-__global__ void __launch_bounds__(kK2Threads) k2_dp_batched(SolveArgs a) {
+#ifndef HEDDLE_K2_MINBLOCKS
+#define HEDDLE_K2_MINBLOCKS 1
+#endif
+__global__ void __launch_bounds__(kK2Threads, HEDDLE_K2_MINBLOCKS) k2_dp_batched(SolveArgs a) {
   using T = Tr<DT, SR>;
   using L = typename T::L;
   using G = typename T::G;

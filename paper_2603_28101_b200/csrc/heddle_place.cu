@@ -18,6 +18,7 @@
 #include "dp_batched.cuh"
 #include "dp_layered.cuh"
 #include "heddle_place.h"
+#include "migration.cuh"
 
 using namespace hp;
 
@@ -1096,6 +1097,19 @@ int64_t heddle_place_debug_violations(void) {
 #else
   return -1;
 #endif
+}
+
+
+heddle_status heddle_place_retarget(const int32_t* boundaries, int32_t m, int32_t B, const int32_t* n_active,
+                                    const int32_t* query_problem, const int32_t* query_rank, int32_t nq,
+                                    int32_t* worker_out, void* stream) {
+  if (!boundaries || !n_active || !query_problem || !query_rank || !worker_out || m < 1 || B < 1 || nq < 0)
+    return HEDDLE_E_INVALID;
+  if (nq == 0) return HEDDLE_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int grid = (int)std::min<int64_t>((nq + 255) / 256, 4096);
+  k6_retarget<<<grid, 256, 0, s>>>(boundaries, m, B, n_active, query_problem, query_rank, nq, worker_out);
+  return cudaGetLastError() == cudaSuccess ? HEDDLE_OK : HEDDLE_E_CUDA;
 }
 
 }  // extern "C"
