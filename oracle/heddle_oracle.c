@@ -355,24 +355,28 @@ int ora_feasible(const ora_problem* p, double X) {
   const int n = p->n, m = p->m;
   int64_t* Wp = weight_prefix(p);
   double* Sp = token_prefix(p);
-  int lo = 0, hi = 0, ok = 1;
+  int lo = 0, hi = 0, ok = 1, interval = 1;
   for (int j = 1; j <= m && ok; ++j) {
-    int nlo = -1, nhi = -1;
+    int nlo = -1, nhi = -1, gap = 0;
     for (int e = lo + 1; e <= n; ++e) {
       int a = hi < e - 1 ? hi : e - 1;
       double c = group_cost_w(p, Wp, Sp, j, a, e);
       if (c != ORA_INF && c <= X) {                /* inadmissible groups never fit */
         if (nlo < 0) nlo = e;
+        if (gap) interval = 0;                     /* true after a false after a true */
         nhi = e;
+      } else if (nlo >= 0) {
+        gap = 1;
       }
     }
     if (nlo < 0) ok = 0;
     lo = nlo; hi = nhi;
   }
-  int res = ok && lo <= n && n <= hi;
-  /* R_j is an interval, so n in [lo, hi] means n in R_m. */
   free(Wp); free(Sp);
-  return res;
+  /* With unit weights the single-item cost c(e-1, e) is non-increasing in e, which makes every
+   * R_j an interval; item weights (aggregation) can break that, and then the test is undecided. */
+  if (!interval) return -1;
+  return ok && lo <= n && n <= hi;
 }
 
 /* Smallest X with feasible(X), by bisection over the ordered bit patterns of
@@ -380,7 +384,10 @@ int ora_feasible(const ora_problem* p, double X) {
 int ora_parametric_opt(const ora_problem* p, double* opt) {
   if (!valid_problem(p)) return ORA_INVALID;
   if (p->semiring != ORA_MINMAX) return ORA_INVALID;
-  if (p->n < p->m || !ora_feasible(p, ORA_INF)) { *opt = ORA_INF; return ORA_INFEASIBLE; }
+  if (p->n < p->m) { *opt = ORA_INF; return ORA_INFEASIBLE; }
+  { const int f = ora_feasible(p, ORA_INF);
+    if (f < 0) return ORA_INVALID;
+    if (!f) { *opt = ORA_INF; return ORA_INFEASIBLE; } }
   uint64_t lo = 0, hi;
   double inf = ORA_INF;
   memcpy(&hi, &inf, sizeof(hi));
@@ -389,7 +396,9 @@ int ora_parametric_opt(const ora_problem* p, double* opt) {
     uint64_t mid = lo + (hi - lo) / 2;
     double x;
     memcpy(&x, &mid, sizeof(x));
-    if (ora_feasible(p, x)) hi = mid; else lo = mid + 1;
+    const int f = ora_feasible(p, x);
+    if (f < 0) return ORA_INVALID;                 /* non-interval R_j: not decidable this way */
+    if (f) hi = mid; else lo = mid + 1;
   }
   memcpy(opt, &hi, sizeof(*opt));
   return ORA_OK;

@@ -127,6 +127,9 @@ def test_parametric_equals_dp_minmax():
         p = oracle.Problem.from_batch(b, 0)
         r = oracle.solve(p)
         q = oracle.parametric_opt(p)
+        if q["status"] == oracle.INVALID:   # weighted items can make R_j a non-interval: undecided
+            assert b.weights is not None, s
+            continue
         assert q["status"] == r["status"], s
         assert q["opt"] == r["opt"], (s, q, r["opt"])
     for s in range(6):  # medium: synthetic rollout-shaped problems
