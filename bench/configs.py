@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--kernel", default="auto")
     ap.add_argument("--dtype", default=None, help="override: f32 / f64 / u32 (integer profile, rounded lengths)")
     ap.add_argument("--semiring", default="minmax")
+    ap.add_argument("--objective", action="store_true", help="time the objective-only parametric kernel (N3)")
     args = ap.parse_args()
     import torch
 
@@ -60,6 +61,24 @@ def main():
         dt = {"u32": torch.uint32, "f32": torch.float32, "f64": torch.float64}[b.profile.dtype]
         L = torch.from_numpy(b.lengths).to(dt).cuda()
         D = torch.from_numpy(b.degrees.astype(np.int32)).cuda()
+        if args.objective:
+            for _ in range(2):
+                pl.objective(L, D)
+            torch.cuda.synchronize()
+            ts_ = []
+            for _ in range(args.reps):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                pl.objective(L, D)
+                e1.record()
+                torch.cuda.synchronize()
+                ts_.append(e0.elapsed_time(e1) / 1e3)
+            t = float(np.median(ts_))
+            print(json.dumps({"config": name, "n": b.n, "m": b.m, "B": b.B, "kernel": "k7_parametric (objective only)",
+                              "ms": 1e3 * t, "solves_per_s": b.B / t,
+                              "dp_equivalent_cells_per_s": b.B * _lib.transitions(b.n, b.m) / t}), flush=True)
+            pl.close()
+            continue
         for _ in range(2):
             pl.solve(L, D)
             pl.backtrack()

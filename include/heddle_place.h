@@ -190,6 +190,16 @@ heddle_status heddle_place_init_split(const heddle_place_config* cfg, const void
                                       int32_t world, heddle_place_ctx** out);
 int32_t heddle_place_split_blocks(int32_t ncb, int32_t world, int32_t rank, int32_t* blocks_out, int32_t cap);
 
+/* Objective only, min-max: the exact optimum dp[m][n] of each problem, bit-identical
+ * to heddle_place_solve's objective, found without the O(n^2 m) DP: bisection over the ordered
+ * values of X with an O(m log n) feasibility test (R_j = prefix ends coverable by exactly j groups
+ * each costing <= X is an interval because the group cost is monotone in both ends; DESIGN.md §5
+ * P6).  No partition is produced (backtrack after it returns E_STATE).  One warp per problem.
+ * E_INVALID for HEDDLE_MINPLUS contexts, weighted items (the interval argument needs unit
+ * weights) and split-mode contexts.  Same per-problem status_out / +inf conventions as solve. */
+heddle_status heddle_place_objective(heddle_place_ctx* ctx, const heddle_place_problem* prob, void* objective_out,
+                                     int32_t* status_out, void* stream);
+
 /* Migration retarget (§5.3).  For each query q: problem
  * query_problem[q] with plan boundaries[b][0..m] (from heddle_place_backtrack; n = b_m), n_active[b]
  * remaining active trajectories n*, and the trajectory's 0-based rank among them by updated

@@ -27,7 +27,8 @@ SEMIRINGS = {"minmax": MINMAX, "minplus": MINPLUS}
 SYMBOLS = ("heddle_place_init", "heddle_place_solve", "heddle_place_backtrack", "heddle_place_solve_host",
            "heddle_place_launch_count", "heddle_place_transitions", "heddle_place_destroy",
            "heddle_place_strerror", "heddle_place_nccl_unique_id", "heddle_place_init_split",
-           "heddle_place_split_blocks", "heddle_place_debug_violations", "heddle_place_retarget")
+           "heddle_place_split_blocks", "heddle_place_debug_violations", "heddle_place_retarget",
+           "heddle_place_objective")
 
 
 class Config(ctypes.Structure):
@@ -87,6 +88,8 @@ def lib() -> ctypes.CDLL:
         L.heddle_place_init_split.restype = ctypes.c_int
         L.heddle_place_split_blocks.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, vp, ctypes.c_int32]
         L.heddle_place_split_blocks.restype = ctypes.c_int32
+        L.heddle_place_objective.argtypes = [vp, ctypes.POINTER(Problem), vp, vp, vp]
+        L.heddle_place_objective.restype = ctypes.c_int
         L.heddle_place_retarget.argtypes = [vp, ctypes.c_int32, ctypes.c_int32, vp, vp, vp, ctypes.c_int32, vp, vp]
         L.heddle_place_retarget.restype = ctypes.c_int
         L.heddle_place_debug_violations.argtypes = []

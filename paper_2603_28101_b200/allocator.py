@@ -137,10 +137,13 @@ class SAResult:
 class ResourceManager:
     """Batched-GPU evaluator for the SA walk.  One Placer (max_batch = chains)."""
 
-    def __init__(self, profile, n_max, m_max, chains, device=None):
+    def __init__(self, profile, n_max, m_max, chains, device=None, objective_only=False):
+        """objective_only: evaluate makespans with the exact parametric kernel (heddle_place_objective,
+        N3) instead of the full DP; the best allocation's partition is solved by the DP at the end."""
         self.placer = Placer.from_profile(profile, max_n=n_max, max_m=m_max, max_batch=chains, device=device)
         self.dev = self.placer.device
         self.evaluations = 0
+        self.objective_only = objective_only
 
     def makespans(self, L, states):
         """PresortedDP makespan of each degree multiset (sorted mapping); one batched
@@ -157,10 +160,13 @@ class ResourceManager:
                 continue
             deg = torch.tensor([states[i] for i in idxs], dtype=torch.int32, device=self.dev)
             Lb = L.reshape(1, n).expand(len(idxs), n)
-            obj, st = self.placer.solve(Lb, deg)
-            bnd = self.placer.backtrack()
+            if self.objective_only:
+                obj, st = self.placer.objective(Lb, deg)
+                bnds = [None] * len(idxs)
+            else:
+                obj, st = self.placer.solve(Lb, deg)
+                bnds = self.placer.backtrack().cpu().numpy()
             objs = obj.double().cpu().numpy()
-            bnds = bnd.cpu().numpy()
             self.evaluations += len(idxs)
             for r, i in enumerate(idxs):
                 out[i] = (float(objs[r]), bnds[r])
@@ -200,5 +206,11 @@ class ResourceManager:
                 T[c] *= cfg.cooling
             it += 1
         b = min(range(P), key=lambda c: (best[c][0], c))
-        return SAResult(best[b][1], best[b][0], best[b][2], it, self.evaluations,
+        bounds = best[b][2]
+        if bounds is None and math.isfinite(best[b][0]):   # objective-only walk: one DP for the partition
+            saved, self.objective_only = self.objective_only, False
+            bounds = self.makespans(L, [best[b][1]])[0][1]
+            self.evaluations -= 1
+            self.objective_only = saved
+        return SAResult(best[b][1], best[b][0], bounds, it, self.evaluations,
                         [(x[0], x[1]) for x in best], trace)

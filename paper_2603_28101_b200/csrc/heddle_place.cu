@@ -19,6 +19,7 @@
 #include "dp_layered.cuh"
 #include "heddle_place.h"
 #include "migration.cuh"
+#include "parametric.cuh"
 
 using namespace hp;
 
@@ -1109,6 +1110,61 @@ heddle_status heddle_place_retarget(const int32_t* boundaries, int32_t m, int32_
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int grid = (int)std::min<int64_t>((nq + 255) / 256, 4096);
   k6_retarget<<<grid, 256, 0, s>>>(boundaries, m, B, n_active, query_problem, query_rank, nq, worker_out);
+  return cudaGetLastError() == cudaSuccess ? HEDDLE_OK : HEDDLE_E_CUDA;
+}
+
+
+heddle_status heddle_place_objective(heddle_place_ctx* x, const heddle_place_problem* p, void* objective_out,
+                                     int32_t* status_out, void* stream) {
+  if (!x || !p || !objective_out || !p->lengths || !p->degrees) return HEDDLE_E_INVALID;
+  if (p->n < 1 || p->m < 1 || p->B < 1 || p->n > x->max_n || p->m > x->max_m || p->B > x->max_batch)
+    return HEDDLE_E_INVALID;
+  if (x->semiring != HEDDLE_MINMAX || p->weights || x->split_world > 1) return HEDDLE_E_INVALID;
+  if (p->lengths_stride < 0 || p->degrees_stride < 0 || p->caps_stride < 0 || p->kv_caps_stride < 0)
+    return HEDDLE_E_INVALID;
+  DeviceGuard guard(x->device);
+  SolveArgs a{};
+  a.n = p->n;
+  a.m = p->m;
+  a.B = p->B;
+  a.lengths = p->lengths;
+  a.ls = p->lengths_stride;
+  a.degrees = p->degrees;
+  a.ds = p->degrees_stride;
+  a.caps = p->caps;
+  a.cs = p->caps_stride;
+  a.kv = p->kv_caps;
+  a.kvs = p->kv_caps_stride;
+  a.gtab = x->d_gtab;
+  a.gstride = x->gstride;
+  a.prof_deg = x->d_prof_deg;
+  a.D = x->D;
+  a.lmax_u32 = x->lmax_u32;
+  a.spws = x->d_sp;
+  a.status = x->d_status;
+  a.status_out = status_out;
+  a.objective = objective_out;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const bool kv = p->kv_caps != nullptr;
+  const int grid = (p->B + kK7Warps - 1) / kK7Warps;
+  // few problems: a CTA of 32 warps per problem (32-ary bisection); many: a warp per problem
+  const bool wide = p->B < 4 * x->num_sms;
+#define HP_K7(DT_)                                                                                 \
+  do {                                                                                             \
+    if (wide) {                                                                                    \
+      if (kv) k7_parametric<DT_, true, 32><<<p->B, 1024, 0, s>>>(a);                              \
+      else k7_parametric<DT_, false, 32><<<p->B, 1024, 0, s>>>(a);                                \
+    } else {                                                                                       \
+      if (kv) k7_parametric<DT_, true, 1><<<grid, 32 * kK7Warps, 0, s>>>(a);                      \
+      else k7_parametric<DT_, false, 1><<<grid, 32 * kK7Warps, 0, s>>>(a);                        \
+    }                                                                                              \
+  } while (0)
+  if (x->dtype == HEDDLE_F32) HP_K7(HEDDLE_F32);
+  else if (x->dtype == HEDDLE_F64) HP_K7(HEDDLE_F64);
+  else HP_K7(HEDDLE_U32);
+#undef HP_K7
+  x->launches++;
+  x->solved = false;   // no dp rows: a following backtrack is a state error
   return cudaGetLastError() == cudaSuccess ? HEDDLE_OK : HEDDLE_E_CUDA;
 }
 

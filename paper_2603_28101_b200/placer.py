@@ -138,6 +138,18 @@ class Placer:
         self._last = (keep, B, n, m)  # keep inputs alive until backtrack
         return obj, st
 
+    def objective(self, lengths, degrees, caps=None, kv_caps=None, stream=None):
+        """Exact min-max optimum only (no partition), by the parametric search kernel (N3):
+        bit-identical to solve()'s objective at O(m log n) probes per bisection step."""
+        p, keep, B, n, m = self._problem(lengths, degrees, caps, kv_caps)
+        obj = torch.empty(B, dtype=self.objective_dtype, device=self.device)
+        st = torch.empty(B, dtype=torch.int32, device=self.device)
+        s = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        C.check(C.lib().heddle_place_objective(self._h, ctypes.byref(p), _ptr(obj), _ptr(st), ctypes.c_void_p(s)),
+                "heddle_place_objective")
+        self._keep_obj = keep
+        return obj, st
+
     def backtrack(self, parents=False, stream=None):
         """Boundaries [B, m+1] (and parents [B, m, n+1] when requested) of the last solve."""
         if self._last is None:

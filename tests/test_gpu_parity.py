@@ -355,6 +355,11 @@ def test_sa_gpu_matches_oracle_sa():
         assert cb == oc and nb == on and gtrace == otrace
     ref = oracle.solve(oracle.Problem(L, prof.T, prof.F, prof.row_of(list(N)), mode="f32"))
     assert np.array_equal(res.best_boundaries, ref["bounds"])
+    # the same walk with the exact objective-only (parametric, N3) evaluator
+    rm2 = alloc.ResourceManager(prof, n_max=256, m_max=40, chains=6, objective_only=True)
+    res2 = rm2.anneal(L, cfg, iu, su)
+    assert res2.best_makespan == c and res2.best_degrees == N and res2.trace == res.trace
+    assert np.array_equal(res2.best_boundaries, ref["bounds"])
 
 
 @pytest.mark.parametrize("kernel", ["layered", "batched", "auto"])
@@ -419,3 +424,44 @@ def test_aggregated_rollout_matches_weighted_oracle():
         assert g["obj"][0] >= exact["opt"]
         full = expand_boundaries(g["bounds"][0], st)
         assert full[0] == 0 and full[-1] == b.n and np.all(np.diff(full) > 0)
+
+
+# ------------------------------------------------------------------ N3: objective-only parametric solver
+@pytest.mark.parametrize("dtype", ["u32", "f32", "f64"])
+def test_objective_parametric_random_tiny(dtype):
+    """The parametric kernel's optimum equals the DP optimum bit for bit (U32 / F32 against the
+    oracle in the same arithmetic; F64 against the GPU DP, same Tr<> arithmetic), incl. caps,
+    kv caps, ties, infeasible and invalid problems."""
+    for s in range(150):
+        batch = wl.tiny_random(s, n_max=20, m_max=6, allow_caps=True, allow_kv=True, dtype=dtype)
+        g = run_gpu(batch)
+        pl = g["placer"]
+        L = to_dev(batch.lengths, {"u32": torch.uint32, "f32": torch.float32, "f64": torch.float64}[dtype])
+        D = to_dev(batch.degrees.astype(np.int32))
+        caps = None if batch.caps is None else to_dev(batch.caps.astype(np.int32))
+        kv = None if batch.kv_caps is None else to_dev(batch.kv_caps.astype(np.int64))
+        obj, st = pl.objective(L, D, caps=caps, kv_caps=kv)
+        torch.cuda.synchronize()
+        o = obj.cpu().numpy().astype(np.float64)
+        assert int(st.cpu()[0]) == int(g["status"][0]), s
+        assert o[0] == g["obj"][0], (s, o[0], g["obj"][0])
+        if dtype != "f64":
+            ref = oracle.solve(oracle.Problem.from_batch(batch, 0, mode=dtype))
+            if ref["status"] == oracle.OK:
+                assert o[0] == ref["opt"], s
+        pl.close()
+
+
+def test_objective_parametric_batched_and_large():
+    """Whole batched launch (16384 problems) and the n = 65536, m = 256 instance: parametric
+    objectives identical to the DP's, problem by problem."""
+    from paper_2603_28101_b200.placer import Placer
+    for batch in (wl.config_batched(), wl.config_large()):
+        g = run_gpu(batch)
+        L = to_dev(batch.lengths)
+        D = to_dev(batch.degrees.astype(np.int32))
+        obj, st = g["placer"].objective(L, D)
+        torch.cuda.synchronize()
+        assert np.all(st.cpu().numpy() == 0)
+        assert np.array_equal(obj.cpu().numpy().astype(np.float64), g["obj"])
+        g["placer"].close()
