@@ -275,7 +275,8 @@ K5Fn pick_k5() { return k5_persistent<DT, SR>; }
 heddle_status solve_persistent(heddle_place_ctx* x, SolveArgs& a, cudaStream_t s) {
   const int dt = x->dtype, sr = x->semiring;
   const int n = a.n, m = a.m, B = a.B, world = x->split_world, rank = x->split_rank;
-  const int kc = k5_kc(n, m, B, x->num_sms, world);
+  int kc = k5_kc(n, m, B, x->num_sms, world);
+  if (const char* e = std::getenv("HEDDLE_PLACE_K5_KC")) kc = std::max(64, std::atoi(e) & ~15);   // tuning
   const int ncb = (n - m + 3) / kK3Cols + 1;
   const int ncb_max = (x->max_n + 3) / kK3Cols + 2;
   if (!x->d_ready) {
