@@ -153,6 +153,12 @@ heddle_status heddle_place_backtrack(heddle_place_ctx* ctx, int32_t* boundaries_
  * pointers, same layout as heddle_place_problem) to the device, solves,
  * backtracks, copies objective / boundaries / status back to host memory and
  * synchronises `stream`.  Pinned host memory makes the copies asynchronous.
+ * When the batched kernel serves the call and B >= 512, the inputs are
+ * pipelined: they are copied on an internal copy stream in chunks (~B/16
+ * problems, >= 256), each chunk followed by a 4-byte ready flag, and the single
+ * solve launch on `stream` starts at once, each CTA waiting for its problem's
+ * chunk -- only the first chunk's copy is exposed.  The context's staging and
+ * flags are reused: one solve_host at a time per context.
  * bytes_h2d / bytes_d2h (may be NULL) receive the bytes copied each way. */
 heddle_status heddle_place_solve_host(heddle_place_ctx* ctx, const heddle_place_problem* host_prob,
                                       void* objective_host, int32_t* boundaries_host,

@@ -71,7 +71,18 @@ struct SolveArgs {
   int32_t* status_out;     // [B] caller's status or null
   void* objective;         // [B] caller's objective
   int* err;                // split mode: set by a peer-exchange timeout (reported as E_NCCL), or null
+  // host-input pipeline (heddle_place_solve_host): problem b's inputs are resident once
+  // ready[b / ready_chunk] == ready_epoch (written by the copy engine after the chunk's copies); null: resident
+  const unsigned* ready;
+  unsigned ready_epoch;
+  int ready_chunk;
 };
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 __host__ __device__ inline int align4(int x) { return (x + 3) & ~3; }
 
@@ -337,9 +348,17 @@ __global__ void __launch_bounds__(kK2Threads, HEDDLE_K2_MINBLOCKS) k2_dp_batched
   const G* gtab = reinterpret_cast<const G*>(a.gtab);
 
   // ---------------- load + validate (lengths sorted/finite/positive, degrees known and sorted)
-  if (tid == 0) s_err = INT_MAX;
+  if (tid == 0) {
+    s_err = INT_MAX;
+    if (a.ready) {   // wait for this problem's chunk of host inputs (copy engine, other stream)
+      const unsigned* f = a.ready + b / a.ready_chunk;
+      while (ld_acquire_u32(f) != a.ready_epoch) __nanosleep(256);
+    }
+  }
   __syncthreads();
-  for (int t = tid; t < n; t += kK2Threads) sL[t] = gL[t];                       // coalesced, batched
+  // inputs are read once, through L2 (ld.cg): a line shared with a neighbour problem whose chunk
+  // is still in flight must not be served later from a stale L1 copy
+  for (int t = tid; t < n; t += kK2Threads) sL[t] = __ldcg(gL + t);               // coalesced, batched
   for (int t = n + tid; t < align4(n + kLPad); t += kK2Threads) sL[t] = (L)1;  // finite pad: no 0*inf
   __syncthreads();
   for (int t = tid; t < n; t += kK2Threads) {
@@ -351,14 +370,14 @@ __global__ void __launch_bounds__(kK2Threads, HEDDLE_K2_MINBLOCKS) k2_dp_batched
     else if (t + 1 < n && sL[t + 1] > x) atomicMin(&s_err, (int)HEDDLE_E_UNSORTED);
   }
   for (int j = tid; j < m; j += kK2Threads) {
-    const int d = a.degrees[(int64_t)b * a.ds + j];
+    const int d = __ldcg(a.degrees + (int64_t)b * a.ds + j);
     int row = -1;
     for (int q = 0; q < a.D; ++q) row = (a.prof_deg[q] == d) ? q : row;
     if (row < 0) atomicMin(&s_err, (int)HEDDLE_E_UNKNOWN_DEGREE);
-    if (j + 1 < m && a.degrees[(int64_t)b * a.ds + j + 1] > d) atomicMin(&s_err, (int)HEDDLE_E_UNSORTED);
+    if (j + 1 < m && __ldcg(a.degrees + (int64_t)b * a.ds + j + 1) > d) atomicMin(&s_err, (int)HEDDLE_E_UNSORTED);
     srow[j] = row < 0 ? 0 : row;
-    scap[j] = a.caps ? a.caps[(int64_t)b * a.cs + j] : -1;
-    skv[j] = KV ? a.kv[(int64_t)b * a.kvs + j] : -1;
+    scap[j] = a.caps ? __ldcg(a.caps + (int64_t)b * a.cs + j) : -1;
+    skv[j] = KV ? __ldcg(a.kv + (int64_t)b * a.kvs + j) : -1;
   }
   if constexpr (W) {   // weight prefix sums Wp (R5): exact, left to right; sizes must fit the cost table
     if (tid == 0) {
@@ -366,7 +385,7 @@ __global__ void __launch_bounds__(kK2Threads, HEDDLE_K2_MINBLOCKS) k2_dp_batched
       sWp[0] = 0;
       bool ok = true;
       for (int t = 0; t < n; ++t) {
-        const int wt = a.w[(int64_t)b * a.ws + t];
+        const int wt = __ldcg(a.w + (int64_t)b * a.ws + t);
         ok = ok && wt >= 1 && acc <= a.gstride - 1 - wt;
         acc += wt > 0 ? wt : 0;
         sWp[t + 1] = acc;

@@ -45,6 +45,10 @@ __global__ void k1_cost_tables(const void* T, const void* F, int D, int s_max, i
 }
 
 // ------------------------------------------------------------------------ context
+// solve_host input pipeline: about kPipeChunks chunks of at least kPipeMinChunk problems
+constexpr int64_t kPipeChunks = 16;
+constexpr int64_t kPipeMinChunk = 256;
+
 struct heddle_place_ctx {
   int device = 0, dtype = 0, semiring = 0;
   int max_n = 0, max_m = 0, max_batch = 0, D = 0, s_max = 0;
@@ -59,6 +63,11 @@ struct heddle_place_ctx {
   int32_t* d_status = nullptr;
   void* d_stage = nullptr;
   size_t stage_bytes = 0;
+  cudaStream_t copy_stream = nullptr;   // solve_host input pipeline: copy stream, its last event,
+  cudaEvent_t copy_done = nullptr;      // per-chunk ready flags (device) and the call epoch (pinned host)
+  unsigned* d_chunk_ready = nullptr;
+  unsigned* h_epoch = nullptr;
+  unsigned pipe_epoch = 0;
   bool solved = false;
   bool last_kv = false;
   SolveArgs last{};
@@ -634,6 +643,10 @@ void heddle_place_destroy(heddle_place_ctx* ctx) {
   cudaFree(ctx->d_sp);
   cudaFree(ctx->d_status);
   cudaFree(ctx->d_stage);
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+  if (ctx->copy_done) cudaEventDestroy(ctx->copy_done);
+  cudaFree(ctx->d_chunk_ready);
+  if (ctx->h_epoch) cudaFreeHost(ctx->h_epoch);
   cudaFree(ctx->d_klo);
   cudaFree(ctx->d_wp);
   cudaFree(ctx->d_keys);
@@ -771,8 +784,18 @@ heddle_status heddle_place_init(const heddle_place_config* c, heddle_place_ctx**
   return HEDDLE_OK;
 }
 
+static heddle_status solve_impl(heddle_place_ctx* x, const heddle_place_problem* p, void* objective_out,
+                                int32_t* status_out, void* stream, const unsigned* ready, unsigned ready_epoch,
+                                int ready_chunk);
+
 heddle_status heddle_place_solve(heddle_place_ctx* x, const heddle_place_problem* p, void* objective_out,
                                  int32_t* status_out, void* stream) {
+  return solve_impl(x, p, objective_out, status_out, stream, nullptr, 0, 1);
+}
+
+static heddle_status solve_impl(heddle_place_ctx* x, const heddle_place_problem* p, void* objective_out,
+                                int32_t* status_out, void* stream, const unsigned* ready, unsigned ready_epoch,
+                                int ready_chunk) {
   if (!x || !p || !objective_out || !p->lengths || !p->degrees) return HEDDLE_E_INVALID;
   if (p->n < 1 || p->m < 1 || p->B < 1 || p->n > x->max_n || p->m > x->max_m || p->B > x->max_batch)
     return HEDDLE_E_INVALID;
@@ -823,6 +846,10 @@ heddle_status heddle_place_solve(heddle_place_ctx* x, const heddle_place_problem
   a.status = x->d_status;
   a.status_out = status_out;
   a.objective = objective_out;
+  a.ready = layered ? nullptr : ready;   // the pipelined inputs are only ever gated for the batched kernel
+  a.ready_epoch = ready_epoch;
+  a.ready_chunk = ready_chunk;
+  if (layered && ready) return HEDDLE_E_INVALID;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (!layered) {
     k2_for(x->dtype, x->semiring, kp, kv, wt)<<<p->B, kK2Threads, smem2, s>>>(a);
@@ -899,18 +926,67 @@ heddle_status heddle_place_solve_host(heddle_place_ctx* x, const heddle_place_pr
   char *dl = base, *dd = dl + bl, *dc = dd + bd, *dk = dc + bc, *dob = dk + bk, *dbd = dob + bo, *dst = dbd + bb;
   char* dw = dst + bs;
   int64_t h2d = 0, d2h = 0;
-  auto up = [&](void* dst_, const void* src, int64_t rows, int64_t cols, int64_t stride, size_t esz) -> bool {
+  // Pipelined inputs (batched kernel, many problems): the host->device copies run on a copy stream
+  // in chunks of problems, each chunk followed by a 4-byte copy of the call's epoch into its ready
+  // flag; the ONE K2 launch on the caller's stream starts at once and each CTA waits (thread 0,
+  // acquire poll) for its problem's chunk, so only the first chunk's copy is exposed.  Copies run on
+  // the copy engines, never on the SMs the waiting CTAs hold, so the wait always ends.
+  const bool kv = p.kv_caps != nullptr, wt = p.weights != nullptr;
+  const bool batched_path = x->split_world == 1 && (wt || (x->flags & HEDDLE_FORCE_BATCHED) ||
+                            (!(x->flags & HEDDLE_FORCE_LAYERED) &&
+                             k2_smem(x->dtype, x->semiring, p.n, p.m, kv, wt) <= x->k2_smem_max &&
+                             !use_layered(x, p.n, p.m, p.B)));
+  int64_t chunk = std::max<int64_t>(kPipeMinChunk, (B + kPipeChunks - 1) / kPipeChunks);
+  if (const char* e = std::getenv("HEDDLE_PLACE_HOST_CHUNK")) chunk = std::max(1, std::atoi(e));   // tuning
+  const int64_t chunks = batched_path ? (B + chunk - 1) / chunk : 1;
+  const bool pipe = chunks > 1;
+  if (pipe && !x->copy_stream) {
+    bool ok = cudaStreamCreateWithFlags(&x->copy_stream, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaEventCreateWithFlags(&x->copy_done, cudaEventDisableTiming) == cudaSuccess &&
+              cudaMalloc(&x->d_chunk_ready, 4 * (size_t)kPipeChunks * 2) == cudaSuccess &&
+              cudaMemset(x->d_chunk_ready, 0, 4 * (size_t)kPipeChunks * 2) == cudaSuccess &&
+              cudaHostAlloc(&x->h_epoch, 4, cudaHostAllocDefault) == cudaSuccess;
+    if (!ok) { cudaGetLastError(); return HEDDLE_E_CUDA; }
+  }
+  if (pipe && chunks > 2 * kPipeChunks) return HEDDLE_E_INVALID;   // only reachable through the tuning knob
+  cudaStream_t cs = pipe ? x->copy_stream : s;
+  unsigned epoch = 0;
+  if (pipe) {
+    epoch = ++x->pipe_epoch;
+    if (epoch == 0) epoch = ++x->pipe_epoch;     // 0 is the flags' initial value
+    *x->h_epoch = epoch;                    // previous calls synchronised: no copy still reads it
+  }
+  auto up = [&](char* dbase, const void* src, int64_t rows, int64_t cols, int64_t stride, size_t esz, int64_t r0,
+                int64_t r1) -> bool {
     if (rows == 0) return true;
+    if (rows == 1) {   // broadcast row: copied once, with the first chunk
+      if (r0 != 0) return true;
+      r1 = 1;
+    }
     const size_t w = esz * cols;
-    h2d += (int64_t)(w * rows);
-    if (stride == cols || rows == 1)
-      return cudaMemcpyAsync(dst_, src, w * rows, cudaMemcpyHostToDevice, s) == cudaSuccess;
-    return cudaMemcpy2DAsync(dst_, w, src, esz * stride, w, rows, cudaMemcpyHostToDevice, s) == cudaSuccess;
+    h2d += (int64_t)(w * (r1 - r0));
+    const char* hs = static_cast<const char*>(src) + esz * stride * r0;
+    char* dd = dbase + w * r0;
+    if (stride == cols || r1 - r0 == 1)
+      return cudaMemcpyAsync(dd, hs, w * (r1 - r0), cudaMemcpyHostToDevice, cs) == cudaSuccess;
+    return cudaMemcpy2DAsync(dd, w, hs, esz * stride, w, r1 - r0, cudaMemcpyHostToDevice, cs) == cudaSuccess;
   };
-  if (!up(dl, p.lengths, lrows, n, p.lengths_stride, es) || !up(dd, p.degrees, drows, m, p.degrees_stride, 4) ||
-      !up(dc, p.caps, crows, m, p.caps_stride, 4) || !up(dk, p.kv_caps, krows, m, p.kv_caps_stride, 8) ||
-      !up(dw, p.weights, wrows, n, p.weights_stride, 4))
-    return HEDDLE_E_CUDA;
+  if (pipe) {   // the copy stream must not overwrite staging a previous use of stream s still reads
+    if (cudaEventRecord(x->copy_done, s) != cudaSuccess || cudaStreamWaitEvent(cs, x->copy_done, 0) != cudaSuccess)
+      return HEDDLE_E_CUDA;
+  }
+  for (int64_t c = 0; c < chunks; ++c) {
+    const int64_t b0 = c * chunk, b1 = pipe ? std::min(B, b0 + chunk) : B;
+    if (!up(dl, p.lengths, lrows, n, p.lengths_stride, es, b0, b1) ||
+        !up(dd, p.degrees, drows, m, p.degrees_stride, 4, b0, b1) ||
+        !up(dc, p.caps, crows, m, p.caps_stride, 4, b0, b1) ||
+        !up(dk, p.kv_caps, krows, m, p.kv_caps_stride, 8, b0, b1) ||
+        !up(dw, p.weights, wrows, n, p.weights_stride, 4, b0, b1))
+      return HEDDLE_E_CUDA;
+    if (pipe && cudaMemcpyAsync(x->d_chunk_ready + c, x->h_epoch, 4, cudaMemcpyHostToDevice, cs) != cudaSuccess)
+      return HEDDLE_E_CUDA;
+  }
+  if (pipe && cudaEventRecord(x->copy_done, cs) != cudaSuccess) return HEDDLE_E_CUDA;
   heddle_place_problem q = p;
   q.lengths = dl;
   q.lengths_stride = p.lengths_stride == 0 ? 0 : n;
@@ -922,8 +998,14 @@ heddle_status heddle_place_solve_host(heddle_place_ctx* x, const heddle_place_pr
   q.kv_caps_stride = p.kv_caps_stride == 0 ? 0 : m;
   q.weights = p.weights ? reinterpret_cast<const int32_t*>(dw) : nullptr;
   q.weights_stride = p.weights_stride == 0 ? 0 : n;
-  heddle_status st = heddle_place_solve(x, &q, dob, reinterpret_cast<int32_t*>(dst), stream);
-  if (st != HEDDLE_OK) return st;
+  heddle_status st =
+      solve_impl(x, &q, dob, reinterpret_cast<int32_t*>(dst), stream, pipe ? x->d_chunk_ready : nullptr, epoch, (int)chunk);
+  if (st != HEDDLE_OK) {
+    if (pipe) cudaStreamSynchronize(cs);
+    return st;
+  }
+  // stream order for everything after the kernel (the backtrack re-reads lengths; the next call's copies)
+  if (pipe && cudaStreamWaitEvent(s, x->copy_done, 0) != cudaSuccess) return HEDDLE_E_CUDA;
   st = heddle_place_backtrack(x, reinterpret_cast<int32_t*>(dbd), nullptr, stream);
   if (st != HEDDLE_OK) return st;
   bool ok = cudaMemcpyAsync(objective_host, dob, oes * B, cudaMemcpyDeviceToHost, s) == cudaSuccess &&

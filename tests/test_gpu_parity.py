@@ -226,6 +226,33 @@ def test_host_e2e_matches_device():
     assert d2h == 4 * batch.B + 4 * batch.B * (batch.m + 1) + 4 * batch.B
 
 
+@pytest.mark.parametrize("bcast_degrees", [False, True])
+def test_host_e2e_chunked_pipeline(bcast_degrees):
+    """B large enough that solve_host pipelines its copies in chunks (ragged last chunk, broadcast
+    rows copied once): results identical to the device-resident solve of the same problems."""
+    from paper_2603_28101_b200.placer import Placer
+    batch = wl.config_batched(B=1301, seed_problem=4)
+    deg = batch.degrees.astype(np.int32)
+    if bcast_degrees:
+        deg = deg[:1]
+    pl = Placer.from_profile(batch.profile, max_n=batch.n, max_m=batch.m, max_batch=batch.B)
+    obj_d, st_d = pl.solve(to_dev(batch.lengths), to_dev(deg))
+    bnd_d = pl.backtrack().cpu().numpy()
+    obj_d = obj_d.cpu().numpy()
+    Lh = torch.from_numpy(batch.lengths).pin_memory()
+    Dh = torch.from_numpy(deg).pin_memory()
+    obj, bnd, st, h2d, d2h = pl.solve_host(Lh, Dh)
+    assert (st.numpy() == 0).all() and (st_d.cpu().numpy() == 0).all()
+    assert np.array_equal(obj.numpy(), obj_d)
+    assert np.array_equal(bnd.numpy(), bnd_d)
+    assert h2d == batch.lengths.nbytes + deg.nbytes
+    idx = np.array([0, 591, 592, 650, 1300])      # chunk edges and the ragged tail
+    rows = np.stack([batch.profile.row_of(deg[0 if bcast_degrees else b]) for b in idx])
+    opt, bounds, _ = oracle.solve_batch(batch.lengths[idx], batch.profile.T, batch.profile.F, rows, mode="f32")
+    assert np.array_equal(obj.numpy()[idx], opt)
+    assert np.array_equal(bnd.numpy()[idx], bounds)
+
+
 def test_error_paths():
     from paper_2603_28101_b200 import E_INVALID, E_STATE, HeddleError
     from paper_2603_28101_b200.placer import Placer
