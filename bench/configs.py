@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--only", default=None)
     ap.add_argument("--kernel", default="auto")
+    ap.add_argument("--algo", default="scan", help="scan (Eq. 3, every split) / valley (HEDDLE_VALLEY, min-max)")
     ap.add_argument("--dtype", default=None, help="override: f32 / f64 / u32 (integer profile, rounded lengths)")
     ap.add_argument("--semiring", default="minmax")
     ap.add_argument("--objective", action="store_true", help="time the objective-only parametric kernel (N3)")
@@ -57,7 +58,7 @@ def main():
             b.profile = wl.float_profile(dtype="f64")
             b.lengths = b.lengths.astype(np.float64)
         pl = Placer.from_profile(b.profile, max_n=b.n, max_m=b.m, max_batch=b.B, kernel=args.kernel,
-                                 semiring=args.semiring)
+                                 semiring=args.semiring, algo=args.algo)
         dt = {"u32": torch.uint32, "f32": torch.float32, "f64": torch.float64}[b.profile.dtype]
         L = torch.from_numpy(b.lengths).to(dt).cuda()
         D = torch.from_numpy(b.degrees.astype(np.int32)).cuda()
@@ -99,9 +100,9 @@ def main():
         ts = float(np.median(tsolve))
         W = b.B * _lib.transitions(b.n, b.m)
         print(json.dumps({"config": name, "n": b.n, "m": b.m, "B": b.B, "dtype": b.profile.dtype,
-                          "semiring": args.semiring,
+                          "semiring": args.semiring, "algo": args.algo,
                           "ms": 1e3 * t, "ms_solve": 1e3 * ts, "ms_backtrack": 1e3 * (t - ts), "cells": W, "cells_per_s": W / t, "solves_per_s": b.B / t,
-                          "frac_alu_roofline": W / t / peak,
+                          "frac_alu_roofline": W / t / peak if args.algo == "scan" else None,
                           "launches_per_solve": (pl.launches - l0) / args.reps}), flush=True)
         pl.close()
 

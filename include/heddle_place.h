@@ -83,6 +83,14 @@ typedef enum { HEDDLE_MINMAX = 0 /* Eq. 3, default */, HEDDLE_MINPLUS = 1 } hedd
 #define HEDDLE_FORCE_BATCHED 0x2u /* always use the one-CTA-per-problem kernel (E_INVALID if n is
                                      too large for shared memory); default: chosen per call    */
 #define HEDDLE_FORCE_LAYERED 0x4u /* always use the layered multi-CTA-per-problem kernel       */
+#define HEDDLE_VALLEY 0x8u        /* MINMAX only (E_INVALID otherwise): solve by the valley search
+                                     (SURVEY §8f N3).  With L non-increasing and F
+                                     non-decreasing, max(dp[j-1][k], c_i(k)) first falls
+                                     then rises in k, so each state needs O(log n) probes instead
+                                     of a scan of k: O(n m log n) per problem.  Results (objective,
+                                     dp rows, boundaries, parents) are bit-identical to the full
+                                     scan.  One CTA per problem while n fits shared memory (about
+                                     18k F32 items), else one launch per layer.  Not in split mode. */
 
 typedef struct heddle_place_ctx heddle_place_ctx;
 

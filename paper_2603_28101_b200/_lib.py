@@ -18,7 +18,9 @@ MINMAX, MINPLUS = 0, 1
 KEEP_PARENTS = 0x1
 FORCE_BATCHED = 0x2
 FORCE_LAYERED = 0x4
+VALLEY = 0x8
 KERNELS = {"auto": 0, "batched": FORCE_BATCHED, "layered": FORCE_LAYERED}
+ALGOS = {"scan": 0, "valley": VALLEY}   # full scan of the splits (Eq. 3) / valley search (min-max, N3)
 
 DTYPES = {"u32": U32, "f32": F32, "f64": F64}
 SEMIRINGS = {"minmax": MINMAX, "minplus": MINPLUS}

@@ -313,11 +313,105 @@ __device__ __forceinline__ void sweep_weighted(const typename Tr<DT, SR>::L* __r
   }
 }
 
+// ---------------- load + validate one problem into shared memory (K2 and K8): lengths sorted,
+// finite, positive; degrees known and sorted; per-worker profile row / cap / kv cap; token and
+// weight prefix sums (also written to the workspace for the backtrack).  Returns the problem's
+// status; a non-zero status is already recorded (status, objective) and the CTA must return.
+template <int DT, int SR, bool KV, bool W, int NT>
+__device__ __forceinline__ int load_problem(const SolveArgs& a, int b, typename Tr<DT, SR>::L* sL, int* srow,
+                                            int* scap, int64_t* skv, typename SpT<DT>::type* sSp, int* sWp,
+                                            int& s_err) {
+  using T = Tr<DT, SR>;
+  using L = typename T::L;
+  using D = typename T::D;
+  using S = typename SpT<DT>::type;
+  const int n = a.n, m = a.m, tid = threadIdx.x;
+  const L* gL = reinterpret_cast<const L*>(a.lengths) + (int64_t)b * a.ls;
+  // ---------------- load + validate (lengths sorted/finite/positive, degrees known and sorted)
+  if (tid == 0) {
+    s_err = INT_MAX;
+    if (a.ready) {   // wait for this problem's chunk of host inputs (copy engine, other stream)
+      const unsigned* f = a.ready + b / a.ready_chunk;
+      while (ld_acquire_u32(f) != a.ready_epoch) __nanosleep(256);
+    }
+  }
+  __syncthreads();
+  // inputs are read once, through L2 (ld.cg): a line shared with a neighbour problem whose chunk
+  // is still in flight must not be served later from a stale L1 copy
+  for (int t = tid; t < n; t += NT) sL[t] = __ldcg(gL + t);               // coalesced, batched
+  for (int t = n + tid; t < align4(n + kLPad); t += NT) sL[t] = (L)1;  // finite pad: no 0*inf
+  __syncthreads();
+  for (int t = tid; t < n; t += NT) {
+    const L x = sL[t];
+    bool bad_range;
+    if constexpr (DT == HEDDLE_U32) bad_range = (x == 0u) || (x > a.lmax_u32);
+    else bad_range = !(x > (L)0) || !(x < (L)INFINITY);
+    if (bad_range) atomicMin(&s_err, (int)HEDDLE_E_RANGE);
+    else if (t + 1 < n && sL[t + 1] > x) atomicMin(&s_err, (int)HEDDLE_E_UNSORTED);
+  }
+  for (int j = tid; j < m; j += NT) {
+    const int d = __ldcg(a.degrees + (int64_t)b * a.ds + j);
+    int row = -1;
+    for (int q = 0; q < a.D; ++q) row = (a.prof_deg[q] == d) ? q : row;
+    if (row < 0) atomicMin(&s_err, (int)HEDDLE_E_UNKNOWN_DEGREE);
+    if (j + 1 < m && __ldcg(a.degrees + (int64_t)b * a.ds + j + 1) > d) atomicMin(&s_err, (int)HEDDLE_E_UNSORTED);
+    srow[j] = row < 0 ? 0 : row;
+    scap[j] = a.caps ? __ldcg(a.caps + (int64_t)b * a.cs + j) : -1;
+    skv[j] = KV ? __ldcg(a.kv + (int64_t)b * a.kvs + j) : -1;
+  }
+  if constexpr (W) {   // weight prefix sums Wp (R5): exact, left to right; sizes must fit the cost table
+    if (tid == 0) {
+      int acc = 0;
+      sWp[0] = 0;
+      bool ok = true;
+      for (int t = 0; t < n; ++t) {
+        const int wt = __ldcg(a.w + (int64_t)b * a.ws + t);
+        ok = ok && wt >= 1 && acc <= a.gstride - 1 - wt;
+        acc += wt > 0 ? wt : 0;
+        sWp[t + 1] = acc;
+      }
+      if (!ok) atomicMin(&s_err, (int)HEDDLE_E_RANGE);
+    }
+    for (int t = n + 1 + tid; t < align4(n + kLPad); t += NT) sWp[t] = INT_MAX / 2;   // beyond n: size < 0
+  }
+  __syncthreads();
+  int err = s_err == INT_MAX ? 0 : s_err;
+  if (err == 0 && n < m) err = HEDDLE_E_INFEASIBLE;   // S:296
+  if (err != 0) {
+    if (tid == 0) {
+      a.status[b] = err;
+      if (a.status_out) a.status_out[b] = err;
+      if constexpr (DT == HEDDLE_U32 && SR == HEDDLE_MINPLUS)
+        reinterpret_cast<uint64_t*>(a.objective)[b] = ~0ull;
+      else
+        reinterpret_cast<D*>(a.objective)[b] = T::inf();
+    }
+    return err;
+  }
+  if constexpr (KV) {  // token prefix sums, left to right (R6) -- one thread, exact order
+    if (tid == 0) {
+      S acc = 0;
+      sSp[0] = 0;
+      for (int t = 0; t < n; ++t) { acc += (S)sL[t]; sSp[t + 1] = acc; }
+    }
+    __syncthreads();
+    S* gSp = reinterpret_cast<S*>(a.spws) + (int64_t)b * (n + 1);   // for the backtrack
+    for (int t = tid; t <= n; t += NT) gSp[t] = sSp[t];
+  }
+  if constexpr (W) {
+    int32_t* gWp = a.wpws + (int64_t)b * (n + 1);   // for the backtrack
+    for (int t = tid; t <= n; t += NT) gWp[t] = sWp[t];
+  }
+  return 0;
+}
+
 template <int DT, int SR, bool KP, bool KV, bool W = false>
 #ifndef HEDDLE_K2_MINBLOCKS
 #define HEDDLE_K2_MINBLOCKS 1
 #endif
-__global__ void __launch_bounds__(kK2Threads, HEDDLE_K2_MINBLOCKS) k2_dp_batched(SolveArgs a) {
+// 32-bit min-max variants fit 128 registers without spilling: 4 CTAs (16 warps) per SM
+__global__ void __launch_bounds__(kK2Threads, (SR == HEDDLE_MINMAX && DT != HEDDLE_F64) ? 4 : HEDDLE_K2_MINBLOCKS)
+    k2_dp_batched(SolveArgs a) {
   using T = Tr<DT, SR>;
   using L = typename T::L;
   using G = typename T::G;
@@ -342,86 +436,11 @@ __global__ void __launch_bounds__(kK2Threads, HEDDLE_K2_MINBLOCKS) k2_dp_batched
   __shared__ D s_redv[kK2Warps];
   __shared__ int s_redk[kK2Warps];
 
-  const L* gL = reinterpret_cast<const L*>(a.lengths) + (int64_t)b * a.ls;
   D* gdp = reinterpret_cast<D*>(a.dpws) + (int64_t)b * (m + 1) * (n + 1);
   int32_t* gpar = KP ? a.parws + (int64_t)b * (m + 1) * (n + 1) : nullptr;
   const G* gtab = reinterpret_cast<const G*>(a.gtab);
 
-  // ---------------- load + validate (lengths sorted/finite/positive, degrees known and sorted)
-  if (tid == 0) {
-    s_err = INT_MAX;
-    if (a.ready) {   // wait for this problem's chunk of host inputs (copy engine, other stream)
-      const unsigned* f = a.ready + b / a.ready_chunk;
-      while (ld_acquire_u32(f) != a.ready_epoch) __nanosleep(256);
-    }
-  }
-  __syncthreads();
-  // inputs are read once, through L2 (ld.cg): a line shared with a neighbour problem whose chunk
-  // is still in flight must not be served later from a stale L1 copy
-  for (int t = tid; t < n; t += kK2Threads) sL[t] = __ldcg(gL + t);               // coalesced, batched
-  for (int t = n + tid; t < align4(n + kLPad); t += kK2Threads) sL[t] = (L)1;  // finite pad: no 0*inf
-  __syncthreads();
-  for (int t = tid; t < n; t += kK2Threads) {
-    const L x = sL[t];
-    bool bad_range;
-    if constexpr (DT == HEDDLE_U32) bad_range = (x == 0u) || (x > a.lmax_u32);
-    else bad_range = !(x > (L)0) || !(x < (L)INFINITY);
-    if (bad_range) atomicMin(&s_err, (int)HEDDLE_E_RANGE);
-    else if (t + 1 < n && sL[t + 1] > x) atomicMin(&s_err, (int)HEDDLE_E_UNSORTED);
-  }
-  for (int j = tid; j < m; j += kK2Threads) {
-    const int d = __ldcg(a.degrees + (int64_t)b * a.ds + j);
-    int row = -1;
-    for (int q = 0; q < a.D; ++q) row = (a.prof_deg[q] == d) ? q : row;
-    if (row < 0) atomicMin(&s_err, (int)HEDDLE_E_UNKNOWN_DEGREE);
-    if (j + 1 < m && __ldcg(a.degrees + (int64_t)b * a.ds + j + 1) > d) atomicMin(&s_err, (int)HEDDLE_E_UNSORTED);
-    srow[j] = row < 0 ? 0 : row;
-    scap[j] = a.caps ? __ldcg(a.caps + (int64_t)b * a.cs + j) : -1;
-    skv[j] = KV ? __ldcg(a.kv + (int64_t)b * a.kvs + j) : -1;
-  }
-  if constexpr (W) {   // weight prefix sums Wp (R5): exact, left to right; sizes must fit the cost table
-    if (tid == 0) {
-      int acc = 0;
-      sWp[0] = 0;
-      bool ok = true;
-      for (int t = 0; t < n; ++t) {
-        const int wt = __ldcg(a.w + (int64_t)b * a.ws + t);
-        ok = ok && wt >= 1 && acc <= a.gstride - 1 - wt;
-        acc += wt > 0 ? wt : 0;
-        sWp[t + 1] = acc;
-      }
-      if (!ok) atomicMin(&s_err, (int)HEDDLE_E_RANGE);
-    }
-    for (int t = n + 1 + tid; t < align4(n + kLPad); t += kK2Threads) sWp[t] = INT_MAX / 2;   // beyond n: size < 0
-  }
-  __syncthreads();
-  int err = s_err == INT_MAX ? 0 : s_err;
-  if (err == 0 && n < m) err = HEDDLE_E_INFEASIBLE;   // S:296
-  if (err != 0) {
-    if (tid == 0) {
-      a.status[b] = err;
-      if (a.status_out) a.status_out[b] = err;
-      if constexpr (DT == HEDDLE_U32 && SR == HEDDLE_MINPLUS)
-        reinterpret_cast<uint64_t*>(a.objective)[b] = ~0ull;
-      else
-        reinterpret_cast<D*>(a.objective)[b] = T::inf();
-    }
-    return;
-  }
-  if constexpr (KV) {  // token prefix sums, left to right (R6) -- one thread, exact order
-    if (tid == 0) {
-      S acc = 0;
-      sSp[0] = 0;
-      for (int t = 0; t < n; ++t) { acc += (S)sL[t]; sSp[t + 1] = acc; }
-    }
-    __syncthreads();
-    S* gSp = reinterpret_cast<S*>(a.spws) + (int64_t)b * (n + 1);   // for the backtrack
-    for (int t = tid; t <= n; t += kK2Threads) gSp[t] = sSp[t];
-  }
-  if constexpr (W) {
-    int32_t* gWp = a.wpws + (int64_t)b * (n + 1);   // for the backtrack
-    for (int t = tid; t <= n; t += kK2Threads) gWp[t] = sWp[t];
-  }
+  if (load_problem<DT, SR, KV, W, kK2Threads>(a, b, sL, srow, scap, skv, sSp, sWp, s_err) != 0) return;
   for (int t = tid; t < align4(n + kLPad); t += kK2Threads) { sdp0[t] = T::inf(); sdp1[t] = T::inf(); }
 
   // ---------------- layers

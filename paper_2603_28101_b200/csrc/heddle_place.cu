@@ -20,6 +20,7 @@
 #include "heddle_place.h"
 #include "migration.cuh"
 #include "parametric.cuh"
+#include "valley.cuh"
 
 using namespace hp;
 
@@ -74,6 +75,8 @@ struct heddle_place_ctx {
   int64_t launches = 0;
   int smem_optin = 0;
   int k2_smem_max = 0;
+  int k8_smem_max = 0;
+  ValleyWs vws{};                       // K8L range-minimum workspace (allocated on first use)
   int num_sms = 0;
   int32_t* d_klo = nullptr;             // [max_batch][max_n+1] (layered kernel, kv caps)
   int32_t* d_wp = nullptr;              // [max_batch][max_n+1] weight prefix sums (weighted problems)
@@ -198,6 +201,45 @@ int k2_smem(int dt, int sr, int n, int m, bool kv, bool w = false) {
   return sr == HEDDLE_MINMAX ? K2Smem<HEDDLE_U32, HEDDLE_MINMAX>(n, m, kv, w).total : K2Smem<HEDDLE_U32, HEDDLE_MINPLUS>(n, m, kv, w).total;
 }
 
+// K8 / K8L (valley solver, min-max only)
+using K8Fn = void (*)(SolveArgs);
+using K8LFn = void (*)(SolveArgs, int, ValleyWs);
+using K8SFn = void (*)(SolveArgs, int, ValleyWs);
+template <int DT>
+K8Fn pick_k8(bool kp, bool kv, bool w) {
+  if (kp) {
+    if (w) return kv ? k8_valley<DT, true, true, true> : k8_valley<DT, true, false, true>;
+    return kv ? k8_valley<DT, true, true, false> : k8_valley<DT, true, false, false>;
+  }
+  if (w) return kv ? k8_valley<DT, false, true, true> : k8_valley<DT, false, false, true>;
+  return kv ? k8_valley<DT, false, true, false> : k8_valley<DT, false, false, false>;
+}
+K8Fn k8_for(int dt, bool kp, bool kv, bool w) {
+  if (dt == HEDDLE_F32) return pick_k8<HEDDLE_F32>(kp, kv, w);
+  if (dt == HEDDLE_F64) return pick_k8<HEDDLE_F64>(kp, kv, w);
+  return pick_k8<HEDDLE_U32>(kp, kv, w);
+}
+template <int DT>
+K8LFn pick_k8l(bool kp, bool kv) {
+  if (kp) return kv ? k8l_layer<DT, true, true> : k8l_layer<DT, true, false>;
+  return kv ? k8l_layer<DT, false, true> : k8l_layer<DT, false, false>;
+}
+K8LFn k8l_for(int dt, bool kp, bool kv) {
+  if (dt == HEDDLE_F32) return pick_k8l<HEDDLE_F32>(kp, kv);
+  if (dt == HEDDLE_F64) return pick_k8l<HEDDLE_F64>(kp, kv);
+  return pick_k8l<HEDDLE_U32>(kp, kv);
+}
+K8SFn k8ls_for(int dt) {
+  if (dt == HEDDLE_F32) return k8l_sparse<HEDDLE_F32>;
+  if (dt == HEDDLE_F64) return k8l_sparse<HEDDLE_F64>;
+  return k8l_sparse<HEDDLE_U32>;
+}
+int k8_smem(int dt, int n, int m, bool kv, bool w) {
+  if (dt == HEDDLE_F32) return K8Smem<HEDDLE_F32>(n, m, kv, w).total;
+  if (dt == HEDDLE_F64) return K8Smem<HEDDLE_F64>(n, m, kv, w).total;
+  return K8Smem<HEDDLE_U32>(n, m, kv, w).total;
+}
+
 template <int DT, int SR>
 int fill_launch(const SolveArgs& a, int64_t cells, int grid, cudaStream_t s) {
   k3_fill<DT, SR><<<grid, 256, 0, s>>>(a, cells);
@@ -275,6 +317,17 @@ bool use_layered(const heddle_place_ctx* x, int n, int m, int B) {
   const double t3 = std::max((double)B * cells / (30.0 * x->num_sms), (double)m * kK3Cols * std::min(kc, n) / 11.0) +
                     20000.0;
   return t3 < t2;
+}
+
+// Does the one-CTA-per-problem kernel (K2, or K8 with HEDDLE_VALLEY) serve this solve?  (Only
+// those kernels can take pipelined host inputs, see heddle_place_solve_host.)
+bool per_problem_kernel(const heddle_place_ctx* x, int n, int m, int B, bool kv, bool wt) {
+  if (x->split_world > 1) return false;
+  if (x->flags & HEDDLE_VALLEY)   // K8 whenever the problem fits shared memory (weights: must fit)
+    return wt || (!(x->flags & HEDDLE_FORCE_LAYERED) && k8_smem(x->dtype, n, m, kv, false) <= x->k8_smem_max);
+  if (wt || (x->flags & HEDDLE_FORCE_BATCHED)) return true;   // weights: batched kernel only
+  if (x->flags & HEDDLE_FORCE_LAYERED) return false;
+  return k2_smem(x->dtype, x->semiring, n, m, kv, wt) <= x->k2_smem_max && !use_layered(x, n, m, B);
 }
 
 template <int DT, int SR>
@@ -646,6 +699,9 @@ void heddle_place_destroy(heddle_place_ctx* ctx) {
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->copy_done) cudaEventDestroy(ctx->copy_done);
   cudaFree(ctx->d_chunk_ready);
+  cudaFree(ctx->vws.mask);
+  cudaFree(ctx->vws.bm);
+  cudaFree(ctx->vws.sp);
   if (ctx->h_epoch) cudaFreeHost(ctx->h_epoch);
   cudaFree(ctx->d_klo);
   cudaFree(ctx->d_wp);
@@ -678,6 +734,7 @@ heddle_status heddle_place_init(const heddle_place_config* c, heddle_place_ctx**
   if (!c || !c->degrees || !c->T || !c->F) return HEDDLE_E_INVALID;
   if (c->dtype < HEDDLE_U32 || c->dtype > HEDDLE_F64) return HEDDLE_E_INVALID;
   if (c->semiring != HEDDLE_MINMAX && c->semiring != HEDDLE_MINPLUS) return HEDDLE_E_INVALID;
+  if ((c->flags & HEDDLE_VALLEY) && c->semiring != HEDDLE_MINMAX) return HEDDLE_E_INVALID;   // no valley in a sum
   if (c->max_n < 1 || c->max_m < 1 || c->max_batch < 1 || c->num_degrees < 1 || c->s_max < 1) return HEDDLE_E_INVALID;
   if (c->max_n > (1 << 24)) return HEDDLE_E_INVALID;
   for (int d = 0; d < c->num_degrees; ++d) {
@@ -780,8 +837,68 @@ heddle_status heddle_place_init(const heddle_place_config* c, heddle_place_ctx**
       }
       x->k2_smem_max = x->smem_optin - (int)fa.sharedSizeBytes;
     }
+  if (c->flags & HEDDLE_VALLEY) {
+    x->k8_smem_max = x->smem_optin;
+    for (int v = 0; v < 8; ++v) {
+      const void* fn = reinterpret_cast<const void*>(k8_for(x->dtype, v & 1, (v >> 1) & 1, v >> 2));
+      cudaFuncAttributes fa{};
+      if (cudaFuncGetAttributes(&fa, fn) != cudaSuccess ||
+          cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               x->smem_optin - (int)fa.sharedSizeBytes) != cudaSuccess) {
+        heddle_place_destroy(x);
+        return HEDDLE_E_CUDA;
+      }
+      x->k8_smem_max = std::min(x->k8_smem_max, x->smem_optin - (int)fa.sharedSizeBytes);
+    }
+  }
   *out = x;
   return HEDDLE_OK;
+}
+
+// K8L path (valley solver, n too large for shared memory): [fill parents] + prologue (validation,
+// prefix sums, layer 1) + one launch per layer + finaliser.
+heddle_status solve_valley_layered(heddle_place_ctx* x, SolveArgs& a, bool kp, bool kv, cudaStream_t s) {
+  const int dt = x->dtype, sr = x->semiring;
+  const int n = a.n, m = a.m, B = a.B;
+  if (a.w) return HEDDLE_E_INVALID;   // aggregation weights: one-CTA-per-problem kernel only
+  if (kp) {   // parents off the computed region read -1
+    const int64_t cells = (int64_t)B * (m + 1) * (n + 1);
+    const int fill_grid = (int)std::min<int64_t>((cells + 255) / 256, (int64_t)x->num_sms * 16);
+    HP_DISPATCH(fill_launch, a, cells, fill_grid, s);
+    x->launches++;
+  }
+  if (!x->vws.mask) {   // range-minimum workspace, sized for the context's limits
+    const int nbm = vblocks(x->max_n), lvm = vlevels(nbm);
+    const size_t des = dp_elem_size(x->dtype, x->semiring);
+    void* mk = nullptr;
+    void *bm = nullptr, *sp = nullptr;
+    if (cudaMalloc(&mk, 4 * 2 * (size_t)x->max_batch * nbm * kVBlk) != cudaSuccess ||
+        cudaMalloc(&bm, des * 2 * (size_t)x->max_batch * nbm) != cudaSuccess ||
+        cudaMalloc(&sp, des * (size_t)x->max_batch * std::max(1, lvm - 1) * nbm) != cudaSuccess) {
+      cudaGetLastError();
+      cudaFree(mk);
+      cudaFree(bm);
+      cudaFree(sp);
+      return HEDDLE_E_NOMEM;
+    }
+    x->vws = ValleyWs{static_cast<uint32_t*>(mk), bm, sp, nbm, lvm};
+  }
+  pro_for(dt, sr, kp, kv)<<<B, 256, 0, s>>>(a);
+  x->launches++;
+  K8LFn fn = k8l_for(dt, kp, kv);
+  for (int j = 1; j <= m; ++j) {
+    const int ilo = (j == 1) ? 1 : (j == m ? n : j), ihi = (j == 1 || j < m) ? n - m + j : n;
+    const int warps = ((ihi >> 5) - (ilo >> 5) + 1 + 3) / 4;
+    fn<<<dim3((warps + kK8LWarps - 1) / kK8LWarps, B), 32 * kK8LWarps, 0, s>>>(a, j, x->vws);
+    x->launches++;
+    if (j < m) {
+      k8ls_for(dt)<<<B, 1024, 0, s>>>(a, j, x->vws);
+      x->launches++;
+    }
+  }
+  HP_DISPATCH(finalize_launch, a, s);
+  x->launches++;
+  return cudaGetLastError() == cudaSuccess ? HEDDLE_OK : HEDDLE_E_CUDA;
 }
 
 static heddle_status solve_impl(heddle_place_ctx* x, const heddle_place_problem* p, void* objective_out,
@@ -805,16 +922,13 @@ static heddle_status solve_impl(heddle_place_ctx* x, const heddle_place_problem*
   const bool kp = (x->flags & HEDDLE_KEEP_PARENTS) != 0;
   const bool wt = p->weights != nullptr;
   if (wt && p->weights_stride < 0) return HEDDLE_E_INVALID;
-  const int smem2 = k2_smem(x->dtype, x->semiring, p->n, p->m, kv, wt);
-  const bool k2_fits = smem2 <= x->k2_smem_max;
+  const bool valley = (x->flags & HEDDLE_VALLEY) != 0;
+  const int smem2 = valley ? k8_smem(x->dtype, p->n, p->m, kv, wt) : k2_smem(x->dtype, x->semiring, p->n, p->m, kv, wt);
+  const bool fits = smem2 <= (valley ? x->k8_smem_max : x->k2_smem_max);
   const bool wide = (x->dtype == HEDDLE_F64) || (x->dtype == HEDDLE_U32 && x->semiring == HEDDLE_MINPLUS);
-  bool layered;
-  if (x->split_world > 1) layered = true;
-  else if (wt || (x->flags & HEDDLE_FORCE_BATCHED)) layered = false;   // weights: batched kernel only
-  else if (x->flags & HEDDLE_FORCE_LAYERED) layered = true;
-  else layered = !k2_fits || use_layered(x, p->n, p->m, p->B);
-  if (!layered && !k2_fits) return HEDDLE_E_INVALID;   // n too large for the one-CTA-per-problem kernel
-  if (layered && kp && wide) return HEDDLE_E_INVALID;    // packed (value, split) atomics need 32-bit values
+  const bool layered = !per_problem_kernel(x, p->n, p->m, p->B, kv, wt);
+  if (!layered && !fits) return HEDDLE_E_INVALID;   // n too large for the one-CTA-per-problem kernel
+  if (layered && kp && wide && !valley) return HEDDLE_E_INVALID;   // packed (value, split) atomics: 32-bit values
   if (x->split_world > 1 && (!layered || kp)) return HEDDLE_E_INVALID;  // split mode: layered, no parent table
   DeviceGuard guard(x->device);
   SolveArgs a{};
@@ -851,7 +965,15 @@ static heddle_status solve_impl(heddle_place_ctx* x, const heddle_place_problem*
   a.ready_chunk = ready_chunk;
   if (layered && ready) return HEDDLE_E_INVALID;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (!layered) {
+  if (valley) {
+    const heddle_status st = layered ? solve_valley_layered(x, a, kp, kv, s) : HEDDLE_OK;
+    if (st != HEDDLE_OK) return st;
+    if (!layered) {
+      k8_for(x->dtype, kp, kv, wt)<<<p->B, kK8Threads, smem2, s>>>(a);
+      x->launches++;
+      if (cudaGetLastError() != cudaSuccess) return HEDDLE_E_CUDA;
+    }
+  } else if (!layered) {
     k2_for(x->dtype, x->semiring, kp, kv, wt)<<<p->B, kK2Threads, smem2, s>>>(a);
     x->launches++;
     if (cudaGetLastError() != cudaSuccess) return HEDDLE_E_CUDA;
@@ -932,10 +1054,7 @@ heddle_status heddle_place_solve_host(heddle_place_ctx* x, const heddle_place_pr
   // acquire poll) for its problem's chunk, so only the first chunk's copy is exposed.  Copies run on
   // the copy engines, never on the SMs the waiting CTAs hold, so the wait always ends.
   const bool kv = p.kv_caps != nullptr, wt = p.weights != nullptr;
-  const bool batched_path = x->split_world == 1 && (wt || (x->flags & HEDDLE_FORCE_BATCHED) ||
-                            (!(x->flags & HEDDLE_FORCE_LAYERED) &&
-                             k2_smem(x->dtype, x->semiring, p.n, p.m, kv, wt) <= x->k2_smem_max &&
-                             !use_layered(x, p.n, p.m, p.B)));
+  const bool batched_path = per_problem_kernel(x, p.n, p.m, p.B, kv, wt);
   int64_t chunk = std::max<int64_t>(kPipeMinChunk, (B + kPipeChunks - 1) / kPipeChunks);
   if (const char* e = std::getenv("HEDDLE_PLACE_HOST_CHUNK")) chunk = std::max(1, std::atoi(e));   // tuning
   const int64_t chunks = batched_path ? (B + chunk - 1) / chunk : 1;
@@ -1122,7 +1241,7 @@ heddle_status heddle_place_init_split(const heddle_place_config* cfg, const void
                                       int32_t world, heddle_place_ctx** out) {
   if (!out) return HEDDLE_E_INVALID;
   *out = nullptr;
-  if (world < 1 || rank < 0 || rank >= world || (cfg && (cfg->flags & HEDDLE_KEEP_PARENTS)))
+  if (world < 1 || rank < 0 || rank >= world || (cfg && (cfg->flags & (HEDDLE_KEEP_PARENTS | HEDDLE_VALLEY))))
     return HEDDLE_E_INVALID;
   if (nccl_unique_id == nullptr && rank != 0) return HEDDLE_E_INVALID;   // emulation: one process
   heddle_place_config c = *cfg;

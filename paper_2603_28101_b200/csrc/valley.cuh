@@ -1,0 +1,368 @@
+// K8 -- exact "valley" solver for the min-max DP (full dp rows + boundaries).
+//
+// Eq. 3 with (+) = max:  dp[j][i] = min_{k in [j-1, i-1]} max(dp[j-1][k], c_i(k)),
+// c_i(k) = L[k] * G_j(size of items [k, i)) (+inf over a size / token cap, R6).
+//   * c_i(k) is non-increasing in k and non-decreasing in i: L is sorted non-increasing,
+//     G_j is non-decreasing in the size (F non-decreasing, P:560 -- checked at init, E_RANGE),
+//     rounding is monotone, and the caps only forbid large groups.
+//   * A split k is dominated for state i by any k' in (k, i-1] with dp[j-1][k'] <= dp[j-1][k]
+//     (no larger on both terms).  So the minimum is unchanged when dp[j-1][k] is replaced by the
+//     suffix minimum sm_i(k) = min(dp[j-1][k..i-1]), which is non-decreasing in k.
+//   * max(sm_i(k), c_i(k)) therefore falls then rises (a valley): with k* = the first k where
+//     sm_i(k) >= c_i(k),  dp[j][i] = min(sm_i(k*), c_i(k*-1))  -- values of the same candidates,
+//     so bit-identical to the full scan (pinned on the oracle's tables: test P8).
+//   * k* is non-decreasing in i (sm_i shrinks and c_i grows with i): a thread sweeping
+//     consecutive states gallops from the previous k*.
+//   * lowest argmin: every candidate is >= dp[j][i], so it is attained exactly where
+//     c_i(k) <= dp[j][i] (a suffix k >= kappa) and dp[j-1][k] <= dp[j][i]: the first such k.
+// With one MP degree for all workers every dp row is non-decreasing and sm_i(k) = dp[j-1][k];
+// mixed degrees give rows with descents (about half the layers of the batched sweep), so the
+// row minimum is a range-minimum structure: per 32-element block, each element's bitmask of the
+// strict suffix minima of its block prefix (min over [k, e] inside a block = the element at the
+// first set bit >= k of mask[e]), plus a sparse table over the block minima.
+// O(n m log n) per problem instead of O(n^2 m) transitions.  Min-max only (a sum of a rising
+// and a falling sequence has no valley).
+#pragma once
+#include <climits>
+#include <cstdint>
+
+#include "dp_batched.cuh"
+
+namespace hp {
+
+constexpr int kK8Threads = 256;
+constexpr int kVBlk = 32;   // range-minimum block (one 32-bit mask per element)
+
+__host__ __device__ inline int vblocks(int n) { return (n >> 5) + 1; }          // blocks over indices 0..n
+__host__ __device__ inline int vlevels(int nb) { int l = 1; while ((2 << (l - 1)) <= nb) ++l; return l; }  // floor(log2 nb)+1
+
+// Range minimum over the computed region of one dp row (the suffix minimum sm_i(k) = rmq(k, i-1)).
+template <class T>
+struct RowMin {
+  using D = typename T::D;
+  const D* v;              // the row
+  const uint32_t* mask;    // [nb*32]: bit t of mask[e] <=> element (e & ~31) + t is a strict suffix
+                           //   minimum of its block's prefix ending at e
+  const D* bm;             // [nb] block minima (sparse level 0)
+  const D* sp;             // [levels-1][nb] sparse levels >= 1 (level l at sp + (l-1)*nb)
+  int nb;
+  bool mono;               // row non-decreasing on the region: rmq(k, e) = v[k]
+  __device__ __forceinline__ D operator()(int k, int e) const {
+    if (mono) return v[k];
+    const int bk = k >> 5, be = e >> 5;
+    if (bk == be) return v[k + __ffs(mask[e] >> (k & 31)) - 1];
+    D r = T::vmin(v[k + __ffs(mask[(bk << 5) + 31] >> (k & 31)) - 1], v[(be << 5) + __ffs(mask[e]) - 1]);
+    if (be - bk > 1) {
+      const int a0 = bk + 1, cnt = be - 1 - a0 + 1, l = 31 - __clz(cnt);
+      const D* lv = l == 0 ? bm : sp + (int64_t)(l - 1) * nb;
+      r = T::vmin(r, T::vmin(lv[a0], lv[be - 1 - (1 << l) + 1]));
+    }
+    return r;
+  }
+};
+
+// Masks and minimum of one 32-element block: `vals` and `mask` address the block's first
+// element; elements outside [lo, hi] (block-relative) read +inf.
+template <class T>
+__device__ __forceinline__ void block_masks(const typename T::D* vals, int lo, int hi, uint32_t* mask,
+                                            typename T::D* bm) {
+  using D = typename T::D;
+  auto val = [&](int t) -> D { return (t >= lo && t <= hi) ? vals[t] : T::inf(); };
+  uint32_t st = 0;
+  for (int t = 0; t < kVBlk; ++t) {
+    const D x = val(t);
+    while (st) {   // pop the staircase entries not strictly below the new element
+      const int h = 31 - __clz(st);
+      if (val(h) >= x) st &= ~(1u << h); else break;
+    }
+    st |= 1u << t;
+    mask[t] = st;
+  }
+  *bm = val(__ffs(st) - 1);
+}
+
+// The layer's group cost and the valley search, shared by the shared-memory (K8) and the
+// global-memory (K8L) kernels.  Pointers address one problem; sizes are item counts, or weight
+// sums with aggregation weights (R5).
+template <int DT, bool KV, bool W>
+struct Valley {
+  using T = Tr<DT, HEDDLE_MINMAX>;
+  using L = typename T::L;
+  using G = typename T::G;
+  using D = typename T::D;
+  using S = typename SpT<DT>::type;
+  const L* sL;
+  RowMin<T> rm;      // dp[j-1][*] and its range minimum
+  const G* grow;     // worker j's cost-table row
+  const S* sSp;      // token prefix sums (KV)
+  const int* sWp;    // weight prefix sums (W)
+  int ghi;           // largest admissible size (the worker's cap, else the table's end)
+  int64_t kvc;       // token cap or < 0
+  // normalised cost of items [k, i) on worker j (+inf when inadmissible)
+  __device__ __forceinline__ D cost(int k, int i) const {
+    const int s = W ? sWp[i] - sWp[k] : i - k;
+    D v = T::norm(T::comb(T::zero(), sL[k], s <= ghi ? grow[s] : T::gpad()));
+    if constexpr (KV) {
+      if (kvc >= 0 && sSp[i] - sSp[k] > (S)kvc) v = T::inf();
+    }
+    return v;
+  }
+  // dp[j][i] over splits [lo, i-1]; `from` >= lo is a split before which the crossing cannot
+  // lie (the previous state's k*); returns the value, the lowest argmin (if wanted) and k*.
+  template <bool ARG>
+  __device__ __forceinline__ D solve(int lo, int i, int from, int& arg, int& kstar) const {
+    const int hi = i - 1;
+    auto crossed = [&](int k) { return rm(k, hi) >= cost(k, i); };
+    int f = max(lo, from) - 1;   // last split known not crossed (or lo - 1)
+    int t = hi + 1;              // first split known crossed (or hi + 1)
+    int step = 1;
+    for (int p = f + 1; p <= hi; p = f + step, step <<= 1) {   // gallop from `from`
+      if (crossed(p)) { t = p; break; }
+      f = p;
+    }
+    while (t - f > 1) {
+      const int mid = (f + t) >> 1;
+      if (crossed(mid)) t = mid; else f = mid;
+    }
+    kstar = t;
+    D v = (t <= hi) ? rm(t, hi) : T::inf();
+    if (t > lo) v = T::vmin(v, cost(t - 1, i));
+    if constexpr (ARG) {
+      if (v == T::inf()) {
+        arg = -1;
+      } else {   // attained where cost(k) <= v (k >= kappa) and dp[j-1][k] <= v: the first such k
+        int a0 = lo - 1, b0 = hi;              // cost(hi) <= v: the smallest cost
+        while (b0 - a0 > 1) {
+          const int mid = (a0 + b0) >> 1;
+          if (cost(mid, i) <= v) b0 = mid; else a0 = mid;
+        }
+        const int kappa = b0;
+        a0 = kappa - 1;
+        b0 = hi;                               // rm(kappa, hi) <= v
+        while (b0 - a0 > 1) {
+          const int mid = (a0 + b0) >> 1;
+          if (rm(kappa, mid) <= v) b0 = mid; else a0 = mid;
+        }
+        arg = b0;
+      }
+    }
+    return v;
+  }
+};
+
+// Shared-memory carve-up of the one-CTA-per-problem valley kernel (bytes).
+template <int DT>
+struct K8Smem {
+  using T = Tr<DT, HEDDLE_MINMAX>;
+  int lOff, d0Off, d1Off, maskOff, spOff, sspOff, wpOff, rowOff, capOff, kvOff, total;
+  __host__ __device__ K8Smem(int n, int m, bool kv, bool w) {
+    int o = 0;
+    auto take = [&](int bytes) { int at = o; o += (bytes + 15) & ~15; return at; };
+    const int nb = vblocks(n);
+    lOff = take((int)sizeof(typename T::L) * align4(n + kLPad));
+    d0Off = take((int)sizeof(typename T::D) * nb * kVBlk);
+    d1Off = take((int)sizeof(typename T::D) * nb * kVBlk);
+    maskOff = take(4 * nb * kVBlk);
+    spOff = take((int)sizeof(typename T::D) * nb * vlevels(nb));
+    sspOff = kv ? take(8 * (n + 1)) : -1;
+    wpOff = w ? take(4 * align4(n + kLPad)) : -1;
+    rowOff = take(4 * m);
+    capOff = take(4 * m);
+    kvOff = take(8 * m);
+    total = o;
+  }
+};
+
+// ---------------------------------------------------------------------------- K8: one CTA per problem
+template <int DT, bool KP, bool KV, bool W>
+__global__ void __launch_bounds__(kK8Threads, 4) k8_valley(SolveArgs a) {
+  using T = Tr<DT, HEDDLE_MINMAX>;
+  using L = typename T::L;
+  using G = typename T::G;
+  using D = typename T::D;
+  using S = typename SpT<DT>::type;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int n = a.n, m = a.m, b = blockIdx.x, tid = threadIdx.x;
+  const K8Smem<DT> lay(n, m, KV, W);
+  L* sL = reinterpret_cast<L*>(smem + lay.lOff);
+  D* const sdp0 = reinterpret_cast<D*>(smem + lay.d0Off);
+  D* const sdp1 = reinterpret_cast<D*>(smem + lay.d1Off);
+  uint32_t* smask = reinterpret_cast<uint32_t*>(smem + lay.maskOff);
+  D* ssp = reinterpret_cast<D*>(smem + lay.spOff);
+  S* sSp = KV ? reinterpret_cast<S*>(smem + lay.sspOff) : nullptr;
+  int* sWp = W ? reinterpret_cast<int*>(smem + lay.wpOff) : nullptr;
+  int* srow = reinterpret_cast<int*>(smem + lay.rowOff);
+  int* scap = reinterpret_cast<int*>(smem + lay.capOff);
+  int64_t* skv = reinterpret_cast<int64_t*>(smem + lay.kvOff);
+  __shared__ int s_err;
+  if (load_problem<DT, HEDDLE_MINMAX, KV, W, kK8Threads>(a, b, sL, srow, scap, skv, sSp, sWp, s_err) != 0) return;
+  __syncthreads();
+  D* gdp = reinterpret_cast<D*>(a.dpws) + (int64_t)b * (m + 1) * (n + 1);
+  int32_t* gpar = KP ? a.parws + (int64_t)b * (m + 1) * (n + 1) : nullptr;
+  const G* gtab = reinterpret_cast<const G*>(a.gtab);
+  const int nb = vblocks(n);
+
+  for (int j = 1; j <= m; ++j) {
+    D* const prev = (j & 1) ? sdp0 : sdp1;
+    D* const cur = (j & 1) ? sdp1 : sdp0;
+    const int ilo = (j == 1) ? 1 : (j == m ? n : j);
+    const int ihi = (j == 1 || j < m) ? n - m + j : n;   // m == 1: layer 1 is the last (i up to n)
+    bool mono = true;
+    if (j > 1) {
+      // range minimum of row j-1 over its computed region [j-1, n-m+j-1]
+      const int plo = j - 1, phi = n - m + j - 1;
+      bool bad = false;
+      for (int t = plo + tid; t < phi; t += kK8Threads) bad |= prev[t] > prev[t + 1];
+      mono = !__syncthreads_or(bad);
+      if (!mono) {
+        const int blo = plo >> 5, bhi = phi >> 5;
+        for (int blk = blo + tid; blk <= bhi; blk += kK8Threads)
+          block_masks<T>(prev + (blk << 5), plo - (blk << 5), phi - (blk << 5), smask + (blk << 5), ssp + blk);
+        __syncthreads();
+        for (int l = 1; (1 << l) <= bhi - blo + 1; ++l) {   // sparse levels over the block minima
+          const D* src = ssp + (int64_t)(l - 1) * nb;
+          D* dst = ssp + (int64_t)l * nb;
+          for (int blk = blo + tid; blk + (1 << l) - 1 <= bhi; blk += kK8Threads)
+            dst[blk] = T::vmin(src[blk], src[blk + (1 << (l - 1))]);
+          __syncthreads();
+        }
+      }
+    }
+    const int cap = scap[j - 1];
+    Valley<DT, KV, W> V{sL, RowMin<T>{prev, smask, ssp, ssp + nb, nb, mono},
+                        gtab + (int64_t)srow[j - 1] * a.gstride, sSp, sWp,
+                        (cap >= 0 && cap < a.gstride - 1) ? cap : a.gstride - 1, KV ? skv[j - 1] : -1};
+    if (j == 1) {   // dp[1][i] = L(tau_1) * T * F(i)
+      for (int i = ilo + tid; i <= ihi; i += kK8Threads) {
+        const D v = V.cost(0, i);
+        cur[i] = v;
+        if (KP) gpar[(int64_t)(n + 1) + i] = (v == T::inf()) ? -1 : 0;
+      }
+    } else {
+      // contiguous runs of states per thread, so each search gallops from the previous k*
+      const int ns = ihi - ilo + 1;
+      const int per = (ns + kK8Threads - 1) / kK8Threads;
+      const int r0 = ilo + tid * per, r1 = min(ihi, r0 + per - 1);
+      int from = j - 1;
+      for (int i = r0; i <= r1; ++i) {
+        int arg = -1, ks;
+        const D v = V.template solve<KP>(j - 1, i, from, arg, ks);
+        from = ks;
+        cur[i] = v;
+        if (KP) gpar[(int64_t)j * (n + 1) + i] = arg;
+      }
+    }
+    __syncthreads();
+    // the finished row to the workspace (coalesced) for the backtrack; -1 parents off the region
+    for (int i = tid; i <= n; i += kK8Threads) {
+      const bool in = (i >= ilo && i <= ihi);
+      if (in) gdp[(int64_t)j * (n + 1) + i] = cur[i];
+      if (KP && !in) gpar[(int64_t)j * (n + 1) + i] = -1;
+    }
+    // (cur is read as `prev` by layer j+1 and rewritten by layer j+2, after its barriers; the
+    //  masks / sparse levels of row j are built by layer j+1 after this layer's last barrier)
+  }
+  if (tid == 0) {
+    const D obj = ((m & 1) ? sdp1 : sdp0)[n];
+    const int st = (obj == T::inf()) ? (int)HEDDLE_E_INFEASIBLE : (int)HEDDLE_OK;
+    a.status[b] = st;
+    if (a.status_out) a.status_out[b] = st;
+    reinterpret_cast<D*>(a.objective)[b] = obj;
+  }
+}
+
+// ------------------------------------------------------------ K8L: one launch per layer (large n)
+// dp rows live in the workspace (L2-resident per layer).  A warp owns 4 consecutive 32-element
+// blocks of the row (a lane: 4 consecutive states, galloping), then builds their masks and minima
+// for the next layer.  Validation and prefix sums come from the layered prologue.
+constexpr int kK8LRun = 4;
+constexpr int kK8LWarps = 8;
+
+struct ValleyWs {                // K8L range-minimum workspace (per problem, row parity p = j & 1)
+  uint32_t* mask;                // [2][B][nb*32]
+  void* bm;                      // [2][B][nb]        block minima (sparse level 0)
+  void* sp;                      // [B][levels-1][nb] sparse levels >= 1 (rebuilt per row)
+  int nbmax, lvmax;
+};
+
+template <int DT, bool KP, bool KV>
+__global__ void __launch_bounds__(32 * kK8LWarps, 4) k8l_layer(SolveArgs a, int j, ValleyWs w) {
+  using T = Tr<DT, HEDDLE_MINMAX>;
+  using L = typename T::L;
+  using G = typename T::G;
+  using D = typename T::D;
+  using S = typename SpT<DT>::type;
+  __shared__ D s_row[kK8LWarps][128];
+  const int n = a.n, m = a.m, b = blockIdx.y, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (a.status[b] != HEDDLE_OK) return;
+  const int ilo = (j == 1) ? 1 : (j == m ? n : j);
+  const int ihi = (j == 1 || j < m) ? n - m + j : n;
+  const int blk0 = (ilo >> 5) + 4 * (blockIdx.x * kK8LWarps + warp);
+  if ((blk0 << 5) > ihi) return;
+  const int nb = vblocks(n);
+  D* gdp = reinterpret_cast<D*>(a.dpws) + (int64_t)b * (m + 1) * (n + 1);
+  const int d = a.degrees[(int64_t)b * a.ds + j - 1];
+  int row = 0;
+  for (int q = 0; q < a.D; ++q) row = (a.prof_deg[q] == d) ? q : row;
+  const int cap = a.caps ? a.caps[(int64_t)b * a.cs + j - 1] : -1;
+  const int pp = (j - 1) & 1;
+  const RowMin<T> rm{gdp + (int64_t)(j - 1) * (n + 1), w.mask + ((int64_t)pp * a.B + b) * nb * kVBlk,
+                     reinterpret_cast<const D*>(w.bm) + ((int64_t)pp * a.B + b) * nb,
+                     reinterpret_cast<const D*>(w.sp) + (int64_t)b * (w.lvmax - 1) * nb, nb, false};
+  Valley<DT, KV, false> V{reinterpret_cast<const L*>(a.lengths) + (int64_t)b * a.ls, rm,
+                          reinterpret_cast<const G*>(a.gtab) + (int64_t)row * a.gstride,
+                          KV ? reinterpret_cast<const S*>(a.spws) + (int64_t)b * (n + 1) : nullptr, nullptr,
+                          (cap >= 0 && cap < a.gstride - 1) ? cap : a.gstride - 1,
+                          KV ? a.kv[(int64_t)b * a.kvs + j - 1] : -1};
+  const int x0 = (blk0 << 5) + kK8LRun * lane;
+  int from = j - 1;
+#pragma unroll
+  for (int r = 0; r < kK8LRun; ++r) {
+    const int i = x0 + r;
+    D v = T::inf();
+    if (i >= ilo && i <= ihi) {
+      int arg = -1, ks = from;
+      if (j == 1) {
+        v = V.cost(0, i);
+        arg = (v == T::inf()) ? -1 : 0;
+      } else {
+        v = V.template solve<KP>(j - 1, i, from, arg, ks);
+        from = ks;
+      }
+      gdp[(int64_t)j * (n + 1) + i] = v;
+      if (KP) a.parws[((int64_t)b * (m + 1) + j) * (n + 1) + i] = arg;
+    }
+    s_row[warp][kK8LRun * lane + r] = v;
+  }
+  if (j == m) return;   // the last row is never queried
+  __syncwarp();
+  if (lane < 4 && blk0 + lane <= (ihi >> 5)) {   // masks + minimum of block blk0 + lane of row j
+    const int p = j & 1;
+    uint32_t* mk = w.mask + ((int64_t)p * a.B + b) * nb * kVBlk;
+    D* bmj = reinterpret_cast<D*>(w.bm) + ((int64_t)p * a.B + b) * nb;
+    const int blk = blk0 + lane;
+    block_masks<T>(s_row[warp] + 32 * lane, ilo - (blk << 5), ihi - (blk << 5), mk + (blk << 5), bmj + blk);
+  }
+}
+
+// sparse levels >= 1 over the block minima of row j (one CTA per problem)
+template <int DT>
+__global__ void __launch_bounds__(1024) k8l_sparse(SolveArgs a, int j, ValleyWs w) {
+  using T = Tr<DT, HEDDLE_MINMAX>;
+  using D = typename T::D;
+  const int n = a.n, m = a.m, b = blockIdx.x;
+  if (a.status[b] != HEDDLE_OK) return;
+  const int ilo = (j == 1) ? 1 : j, ihi = n - m + j;
+  const int blo = ilo >> 5, bhi = ihi >> 5, nb = vblocks(n);
+  const D* bmj = reinterpret_cast<const D*>(w.bm) + ((int64_t)(j & 1) * a.B + b) * nb;
+  D* sp = reinterpret_cast<D*>(w.sp) + (int64_t)b * (w.lvmax - 1) * nb;
+  for (int l = 1; (1 << l) <= bhi - blo + 1; ++l) {
+    const D* src = l == 1 ? bmj : sp + (int64_t)(l - 2) * nb;
+    D* dst = sp + (int64_t)(l - 1) * nb;
+    for (int blk = blo + threadIdx.x; blk + (1 << l) - 1 <= bhi; blk += blockDim.x)
+      dst[blk] = T::vmin(src[blk], src[blk + (1 << (l - 1))]);
+    __syncthreads();
+  }
+}
+
+}  // namespace hp

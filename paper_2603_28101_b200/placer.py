@@ -45,9 +45,11 @@ class Placer:
     """One heddle_place context: a profile (MP degrees, T, F) and workspace limits."""
 
     def __init__(self, degrees, T, F, *, dtype="f32", semiring="minmax", max_n, max_m, max_batch,
-                 device=None, keep_parents=False, kernel="auto", split=None):
+                 device=None, keep_parents=False, kernel="auto", algo="scan", split=None):
         """split=(unique_id_bytes or None, rank, world): multi-GPU split mode (collective solves);
-        unique_id None with rank 0 runs the single-device emulation of `world` ranks."""
+        unique_id None with rank 0 runs the single-device emulation of `world` ranks.
+        algo: "scan" evaluates every split of Eq. 3; "valley" (min-max only) finds the same
+        values and argmins by the valley search (HEDDLE_VALLEY, O(n m log n))."""
         self.dtype = C.DTYPES[dtype] if isinstance(dtype, str) else dtype
         self.semiring = C.SEMIRINGS[semiring] if isinstance(semiring, str) else semiring
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
@@ -60,7 +62,7 @@ class Placer:
         self._F = np.ascontiguousarray(F.astype(npdt))
         cfg = C.Config(self.device.index, self.dtype, self.semiring, max_n, max_m, max_batch, self._deg.size,
                        self._deg.ctypes.data, self._T.ctypes.data, self._F.ctypes.data, self._F.shape[1],
-                       (C.KEEP_PARENTS if keep_parents else 0) | C.KERNELS[kernel])
+                       (C.KEEP_PARENTS if keep_parents else 0) | C.KERNELS[kernel] | C.ALGOS[algo])
         h = ctypes.c_void_p()
         if split is None:
             C.check(C.lib().heddle_place_init(ctypes.byref(cfg), ctypes.byref(h)), "heddle_place_init")
@@ -71,6 +73,7 @@ class Placer:
                     "heddle_place_init_split")
         self._h = h
         self.keep_parents = keep_parents
+        self.algo = algo
         self.max_n, self.max_m, self.max_batch = max_n, max_m, max_batch
         self._last = None
 

@@ -28,13 +28,14 @@ def to_dev(a, dt=None):
 
 
 def run_gpu(batch, semiring="minmax", keep_parents=False, dtype=None, placer=None, lengths_shared=False,
-            kernel="auto"):
+            kernel="auto", algo="scan"):
     dtype = dtype or batch.profile.dtype
     if placer is None:
         # weighted items: group sizes reach the total weight, which must fit the cost table (max_n)
         max_n = batch.n if batch.weights is None else max(batch.n, int(batch.weights.sum(axis=1).max()))
         placer = Placer(batch.profile.degrees, batch.profile.T, batch.profile.F, dtype=dtype, semiring=semiring,
-                        max_n=max_n, max_m=batch.m, max_batch=batch.B, keep_parents=keep_parents, kernel=kernel)
+                        max_n=max_n, max_m=batch.m, max_batch=batch.B, keep_parents=keep_parents, kernel=kernel,
+                        algo=algo)
     L = to_dev(batch.lengths[:1] if lengths_shared else batch.lengths, TDT[dtype])
     if lengths_shared:
         L = L[0]

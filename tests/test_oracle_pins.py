@@ -261,3 +261,59 @@ def test_generators_long_tail():
     b = wl.config_batched(B=8)
     assert np.all(np.diff(b.lengths.astype(np.float64), axis=1) <= 0)
     assert np.all(np.diff(b.degrees, axis=1) <= 0)
+
+
+# ------------------------------------------------------------------ P8: the valley characterisation
+@pytest.mark.parametrize("mode", ["u32", "f32", "f64"])
+def test_valley_characterisation_on_oracle_tables(mode):
+    """P8 (the premise of the HEDDLE_VALLEY kernels), on the oracle's own tables.
+    With L non-increasing and F non-decreasing:
+      * c_i(k) (cost of items [k, i) on worker j) is non-increasing in k and non-decreasing in i;
+      * with sm_i(k) = min(dp[j-1][k..i-1]) (non-decreasing in k) and k* = the first split with
+        sm_i(k) >= c_i(k):  dp[j][i] = min(sm_i(k*), c_i(k*-1)), and k* is non-decreasing in i;
+      * the lowest argmin is the first e >= kappa with dp[j-1][e] <= dp[j][i], kappa = the first
+        k with c_i(k) <= dp[j][i];
+      * with one MP degree for all workers every computed dp row is non-decreasing in i (the
+        suffix minimum is then the row itself); with mixed degrees it need not be -- a case
+        below must show a descent, so the suffix minimum is really needed.
+    Ties, clamp plateaus, caps, kv caps and weights included (tiny_random)."""
+    checked = descents = 0
+    for s in range(150):
+        batch = wl.tiny_random(s, n_max=18, m_max=6, allow_caps=True, allow_kv=True, allow_weights=(s % 3 == 0),
+                               dtype=mode)
+        p = oracle.Problem.from_batch(batch, 0, mode=mode)
+        r = oracle.solve(p, want_tables=True)
+        if r["status"] not in (oracle.OK, oracle.INFEASIBLE) or batch.n < batch.m:
+            continue
+        dp, par = r["dp"], r["parent"]
+        n, m = batch.n, batch.m
+        homogeneous = len(set(batch.degrees[0].tolist())) == 1
+        for j in range(1, m + 1):
+            row = [dp[j][i] for i in range(j, n - m + j + 1)]
+            mono = all(a <= b for a, b in zip(row, row[1:]))
+            assert mono or not homogeneous, (s, j)
+            descents += not mono
+        for j in range(2, m + 1):
+            last_t = -1
+            for i in (range(j, n - m + j + 1) if j < m else [n]):
+                ks = list(range(j - 1, i))
+                c = [oracle.group_cost(p, j, k, i) for k in ks]
+                assert all(a >= b for a, b in zip(c, c[1:])), (s, j, i)
+                if i > j:
+                    assert all(oracle.group_cost(p, j, k, i - 1) <= ck for k, ck in zip(ks[:-1], c)), (s, j, i)
+                prev = [dp[j - 1][k] for k in ks]
+                sm = [min(prev[q:]) for q in range(len(ks))]
+                t = next((q for q in range(len(ks)) if sm[q] >= c[q]), len(ks))
+                kst = ks[t] if t < len(ks) else i      # (i = none crossed)
+                assert kst >= last_t, (s, j, i)
+                last_t = kst
+                v = sm[t] if t < len(ks) else math.inf
+                if t > 0:
+                    v = min(v, c[t - 1])
+                assert v == dp[j][i], (s, j, i, v, dp[j][i])
+                if v != math.inf:
+                    kappa = next(q for q in range(len(ks)) if c[q] <= v)
+                    arg = next(q for q in range(kappa, len(ks)) if prev[q] <= v)
+                    assert par[j][i] == ks[arg], (s, j, i)
+                checked += 1
+    assert checked > 1000 and descents > 0
