@@ -76,6 +76,7 @@ struct SolveArgs {
   const unsigned* ready;
   unsigned ready_epoch;
   int ready_chunk;
+  int vscan;               // valley kernel: descent prefixes shorter than this are scanned (K8)
 };
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {

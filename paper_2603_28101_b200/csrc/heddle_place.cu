@@ -229,10 +229,10 @@ K8LFn k8l_for(int dt, bool kp, bool kv) {
   if (dt == HEDDLE_F64) return pick_k8l<HEDDLE_F64>(kp, kv);
   return pick_k8l<HEDDLE_U32>(kp, kv);
 }
-K8SFn k8ls_for(int dt) {
-  if (dt == HEDDLE_F32) return k8l_sparse<HEDDLE_F32>;
-  if (dt == HEDDLE_F64) return k8l_sparse<HEDDLE_F64>;
-  return k8l_sparse<HEDDLE_U32>;
+K8SFn k8lr_for(int dt) {
+  if (dt == HEDDLE_F32) return k8l_rowprep<HEDDLE_F32>;
+  if (dt == HEDDLE_F64) return k8l_rowprep<HEDDLE_F64>;
+  return k8l_rowprep<HEDDLE_U32>;
 }
 int k8_smem(int dt, int n, int m, bool kv, bool w) {
   if (dt == HEDDLE_F32) return K8Smem<HEDDLE_F32>(n, m, kv, w).total;
@@ -702,6 +702,8 @@ void heddle_place_destroy(heddle_place_ctx* ctx) {
   cudaFree(ctx->vws.mask);
   cudaFree(ctx->vws.bm);
   cudaFree(ctx->vws.sp);
+  cudaFree(ctx->vws.smd);
+  cudaFree(ctx->vws.dlast);
   if (ctx->h_epoch) cudaFreeHost(ctx->h_epoch);
   cudaFree(ctx->d_klo);
   cudaFree(ctx->d_wp);
@@ -871,17 +873,17 @@ heddle_status solve_valley_layered(heddle_place_ctx* x, SolveArgs& a, bool kp, b
     const int nbm = vblocks(x->max_n), lvm = vlevels(nbm);
     const size_t des = dp_elem_size(x->dtype, x->semiring);
     void* mk = nullptr;
-    void *bm = nullptr, *sp = nullptr;
+    void *bm = nullptr, *sp = nullptr, *smd = nullptr, *dl = nullptr;
     if (cudaMalloc(&mk, 4 * 2 * (size_t)x->max_batch * nbm * kVBlk) != cudaSuccess ||
         cudaMalloc(&bm, des * 2 * (size_t)x->max_batch * nbm) != cudaSuccess ||
-        cudaMalloc(&sp, des * (size_t)x->max_batch * std::max(1, lvm - 1) * nbm) != cudaSuccess) {
+        cudaMalloc(&sp, des * (size_t)x->max_batch * std::max(1, lvm - 1) * nbm) != cudaSuccess ||
+        cudaMalloc(&smd, des * (size_t)x->max_batch * (x->max_n + 1)) != cudaSuccess ||
+        cudaMalloc(&dl, 4 * (size_t)x->max_batch) != cudaSuccess) {
       cudaGetLastError();
-      cudaFree(mk);
-      cudaFree(bm);
-      cudaFree(sp);
+      for (void* q : {mk, bm, sp, smd, dl}) cudaFree(q);
       return HEDDLE_E_NOMEM;
     }
-    x->vws = ValleyWs{static_cast<uint32_t*>(mk), bm, sp, nbm, lvm};
+    x->vws = ValleyWs{static_cast<uint32_t*>(mk), bm, sp, smd, static_cast<int*>(dl), nbm, lvm};
   }
   pro_for(dt, sr, kp, kv)<<<B, 256, 0, s>>>(a);
   x->launches++;
@@ -892,7 +894,7 @@ heddle_status solve_valley_layered(heddle_place_ctx* x, SolveArgs& a, bool kp, b
     fn<<<dim3((warps + kK8LWarps - 1) / kK8LWarps, B), 32 * kK8LWarps, 0, s>>>(a, j, x->vws);
     x->launches++;
     if (j < m) {
-      k8ls_for(dt)<<<B, 1024, 0, s>>>(a, j, x->vws);
+      k8lr_for(dt)<<<B, 1024, 0, s>>>(a, j, x->vws);
       x->launches++;
     }
   }
@@ -960,6 +962,8 @@ static heddle_status solve_impl(heddle_place_ctx* x, const heddle_place_problem*
   a.status = x->d_status;
   a.status_out = status_out;
   a.objective = objective_out;
+  a.vscan = kScanPrefix;
+  if (const char* e = std::getenv("HEDDLE_PLACE_VALLEY_SCAN")) a.vscan = std::atoi(e);   // tests / tuning
   a.ready = layered ? nullptr : ready;   // the pipelined inputs are only ever gated for the batched kernel
   a.ready_epoch = ready_epoch;
   a.ready_chunk = ready_chunk;

@@ -15,11 +15,16 @@
 //     consecutive states gallops from the previous k*.
 //   * lowest argmin: every candidate is >= dp[j][i], so it is attained exactly where
 //     c_i(k) <= dp[j][i] (a suffix k >= kappa) and dp[j-1][k] <= dp[j][i]: the first such k.
-// With one MP degree for all workers every dp row is non-decreasing and sm_i(k) = dp[j-1][k];
-// mixed degrees give rows with descents (about half the layers of the batched sweep), so the
-// row minimum is a range-minimum structure: per 32-element block, each element's bitmask of the
-// strict suffix minima of its block prefix (min over [k, e] inside a block = the element at the
-// first set bit >= k of mask[e]), plus a sparse table over the block minima.
+// With one MP degree for all workers every dp row is non-decreasing and sm_i(k) = dp[j-1][k].
+// Mixed degrees give rows with descents (about half the layers of the batched sweep), but only
+// near the row's start (the slow workers matter only while groups are tiny): with d = the last
+// descent of the row, the row is non-decreasing beyond d, so
+//   sm_i(k) = dp[j-1][k]                        for k > d,
+//           = min(dp[j-1][k..d+1])  (a suffix-minimum array of the short prefix)  for i-1 > d,
+// and only states i <= d+1 need a general range minimum: a linear scan while the prefix is short,
+// else per 32-element block each element's bitmask of the strict suffix minima of its block
+// prefix (min over [k, e] in a block = the element at the first set bit >= k of mask[e]) plus a
+// sparse table over the block minima.
 // O(n m log n) per problem instead of O(n^2 m) transitions.  Min-max only (a sum of a rising
 // and a falling sequence has no valley).
 #pragma once
@@ -31,7 +36,9 @@
 namespace hp {
 
 constexpr int kK8Threads = 256;
-constexpr int kVBlk = 32;   // range-minimum block (one 32-bit mask per element)
+constexpr int kVBlk = 32;        // range-minimum block (one 32-bit mask per element)
+constexpr int kScanPrefix = 96;  // default SolveArgs::vscan: descent prefixes shorter than this are
+                                 // scanned state by state (no masks / sparse table built)
 
 __host__ __device__ inline int vblocks(int n) { return (n >> 5) + 1; }          // blocks over indices 0..n
 __host__ __device__ inline int vlevels(int nb) { int l = 1; while ((2 << (l - 1)) <= nb) ++l; return l; }  // floor(log2 nb)+1
@@ -41,14 +48,16 @@ template <class T>
 struct RowMin {
   using D = typename T::D;
   const D* v;              // the row
+  const D* smd;            // [k] = min(v[k..dlast+1]) for k in [row start, dlast+1]
   const uint32_t* mask;    // [nb*32]: bit t of mask[e] <=> element (e & ~31) + t is a strict suffix
-                           //   minimum of its block's prefix ending at e
+                           //   minimum of its block's prefix ending at e   (e <= dlast only)
   const D* bm;             // [nb] block minima (sparse level 0)
   const D* sp;             // [levels-1][nb] sparse levels >= 1 (level l at sp + (l-1)*nb)
   int nb;
-  bool mono;               // row non-decreasing on the region: rmq(k, e) = v[k]
+  int dlast;               // last descent v[d] > v[d+1] of the region, < row start if none
   __device__ __forceinline__ D operator()(int k, int e) const {
-    if (mono) return v[k];
+    if (k > dlast) return v[k];          // non-decreasing from k on
+    if (e > dlast) return smd[k];        // [k, e] covers d+1, beyond which nothing is smaller
     const int bk = k >> 5, be = e >> 5;
     if (bk == be) return v[k + __ffs(mask[e] >> (k & 31)) - 1];
     D r = T::vmin(v[k + __ffs(mask[(bk << 5) + 31] >> (k & 31)) - 1], v[(be << 5) + __ffs(mask[e]) - 1]);
@@ -60,6 +69,27 @@ struct RowMin {
     return r;
   }
 };
+
+// smd[k] = min(row[k..hi]) for k in [lo, hi], by one warp (suffix scans of 32, right to left)
+template <class T>
+__device__ __forceinline__ void suffix_min_warp(const typename T::D* row, int lo, int hi, typename T::D* smd,
+                                                int lane) {
+  using D = typename T::D;
+  D carry = T::inf();
+  for (int base = hi - 31;; base -= 32) {
+    const int idx = base + lane;
+    D x = (idx >= lo) ? row[idx] : T::inf();
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const D y = __shfl_down_sync(0xffffffffu, x, off);
+      if (lane + off < 32) x = T::vmin(x, y);
+    }
+    x = T::vmin(x, carry);
+    if (idx >= lo) smd[idx] = x;
+    carry = __shfl_sync(0xffffffffu, x, 0);
+    if (base <= lo) break;
+  }
+}
 
 // Masks and minimum of one 32-element block: `vals` and `mask` address the block's first
 // element; elements outside [lo, hi] (block-relative) read +inf.
@@ -98,6 +128,7 @@ struct Valley {
   const int* sWp;    // weight prefix sums (W)
   int ghi;           // largest admissible size (the worker's cap, else the table's end)
   int64_t kvc;       // token cap or < 0
+  bool scan_prefix;  // states i <= dlast+1 scan their splits (short descent prefix: no masks built)
   // normalised cost of items [k, i) on worker j (+inf when inadmissible)
   __device__ __forceinline__ D cost(int k, int i) const {
     const int s = W ? sWp[i] - sWp[k] : i - k;
@@ -112,6 +143,18 @@ struct Valley {
   template <bool ARG>
   __device__ __forceinline__ D solve(int lo, int i, int from, int& arg, int& kstar) const {
     const int hi = i - 1;
+    if (scan_prefix && hi <= rm.dlast) {   // Eq. 3 as written, lowest argmin (strict '<', k ascending)
+      D v = T::inf();
+      int bk = -1;
+      for (int k = lo; k <= hi; ++k) {
+        const D cv = cost(k, i), pv = rm.v[k];
+        const D c = pv > cv ? pv : cv;
+        if (c < v) { v = c; bk = k; }
+      }
+      if constexpr (ARG) arg = (v == T::inf()) ? -1 : bk;
+      kstar = lo;   // no crossing information: the next state searches from lo
+      return v;
+    }
     auto crossed = [&](int k) { return rm(k, hi) >= cost(k, i); };
     int f = max(lo, from) - 1;   // last split known not crossed (or lo - 1)
     int t = hi + 1;              // first split known crossed (or hi + 1)
@@ -137,13 +180,19 @@ struct Valley {
           if (cost(mid, i) <= v) b0 = mid; else a0 = mid;
         }
         const int kappa = b0;
-        a0 = kappa - 1;
-        b0 = hi;                               // rm(kappa, hi) <= v
-        while (b0 - a0 > 1) {
-          const int mid = (a0 + b0) >> 1;
-          if (rm(kappa, mid) <= v) b0 = mid; else a0 = mid;
+        if (scan_prefix && kappa <= rm.dlast) {   // no masks: walk the short descent prefix
+          int e = kappa;                          // (the row is non-decreasing from dlast+1 on, so
+          while (rm.v[e] > v) ++e;                //  the first e with v[e] <= v is at most dlast+1)
+          arg = e;
+        } else {
+          a0 = kappa - 1;
+          b0 = hi;                                // rm(kappa, hi) <= v
+          while (b0 - a0 > 1) {
+            const int mid = (a0 + b0) >> 1;
+            if (rm(kappa, mid) <= v) b0 = mid; else a0 = mid;
+          }
+          arg = b0;
         }
-        arg = b0;
       }
     }
     return v;
@@ -154,7 +203,7 @@ struct Valley {
 template <int DT>
 struct K8Smem {
   using T = Tr<DT, HEDDLE_MINMAX>;
-  int lOff, d0Off, d1Off, maskOff, spOff, sspOff, wpOff, rowOff, capOff, kvOff, total;
+  int lOff, d0Off, d1Off, smdOff, maskOff, spOff, sspOff, wpOff, rowOff, capOff, kvOff, total;
   __host__ __device__ K8Smem(int n, int m, bool kv, bool w) {
     int o = 0;
     auto take = [&](int bytes) { int at = o; o += (bytes + 15) & ~15; return at; };
@@ -162,6 +211,7 @@ struct K8Smem {
     lOff = take((int)sizeof(typename T::L) * align4(n + kLPad));
     d0Off = take((int)sizeof(typename T::D) * nb * kVBlk);
     d1Off = take((int)sizeof(typename T::D) * nb * kVBlk);
+    smdOff = take((int)sizeof(typename T::D) * (n + 1));
     maskOff = take(4 * nb * kVBlk);
     spOff = take((int)sizeof(typename T::D) * nb * vlevels(nb));
     sspOff = kv ? take(8 * (n + 1)) : -1;
@@ -187,6 +237,7 @@ __global__ void __launch_bounds__(kK8Threads, 4) k8_valley(SolveArgs a) {
   L* sL = reinterpret_cast<L*>(smem + lay.lOff);
   D* const sdp0 = reinterpret_cast<D*>(smem + lay.d0Off);
   D* const sdp1 = reinterpret_cast<D*>(smem + lay.d1Off);
+  D* ssmd = reinterpret_cast<D*>(smem + lay.smdOff);
   uint32_t* smask = reinterpret_cast<uint32_t*>(smem + lay.maskOff);
   D* ssp = reinterpret_cast<D*>(smem + lay.spOff);
   S* sSp = KV ? reinterpret_cast<S*>(smem + lay.sspOff) : nullptr;
@@ -194,7 +245,8 @@ __global__ void __launch_bounds__(kK8Threads, 4) k8_valley(SolveArgs a) {
   int* srow = reinterpret_cast<int*>(smem + lay.rowOff);
   int* scap = reinterpret_cast<int*>(smem + lay.capOff);
   int64_t* skv = reinterpret_cast<int64_t*>(smem + lay.kvOff);
-  __shared__ int s_err;
+  __shared__ int s_err, s_dlast[2];
+  if (tid == 0) { s_dlast[0] = -1; s_dlast[1] = -1; }
   if (load_problem<DT, HEDDLE_MINMAX, KV, W, kK8Threads>(a, b, sL, srow, scap, skv, sSp, sWp, s_err) != 0) return;
   __syncthreads();
   D* gdp = reinterpret_cast<D*>(a.dpws) + (int64_t)b * (m + 1) * (n + 1);
@@ -207,31 +259,43 @@ __global__ void __launch_bounds__(kK8Threads, 4) k8_valley(SolveArgs a) {
     D* const cur = (j & 1) ? sdp1 : sdp0;
     const int ilo = (j == 1) ? 1 : (j == m ? n : j);
     const int ihi = (j == 1 || j < m) ? n - m + j : n;   // m == 1: layer 1 is the last (i up to n)
-    bool mono = true;
+    int dl = -1;            // last descent of row j-1 (-1: non-decreasing)
+    bool scan_prefix = false;
     if (j > 1) {
       // range minimum of row j-1 over its computed region [j-1, n-m+j-1]
       const int plo = j - 1, phi = n - m + j - 1;
-      bool bad = false;
-      for (int t = plo + tid; t < phi; t += kK8Threads) bad |= prev[t] > prev[t + 1];
-      mono = !__syncthreads_or(bad);
-      if (!mono) {
-        const int blo = plo >> 5, bhi = phi >> 5;
-        for (int blk = blo + tid; blk <= bhi; blk += kK8Threads)
-          block_masks<T>(prev + (blk << 5), plo - (blk << 5), phi - (blk << 5), smask + (blk << 5), ssp + blk);
-        __syncthreads();
-        for (int l = 1; (1 << l) <= bhi - blo + 1; ++l) {   // sparse levels over the block minima
-          const D* src = ssp + (int64_t)(l - 1) * nb;
-          D* dst = ssp + (int64_t)l * nb;
-          for (int blk = blo + tid; blk + (1 << l) - 1 <= bhi; blk += kK8Threads)
-            dst[blk] = T::vmin(src[blk], src[blk + (1 << (l - 1))]);
+      int myd = -1;
+      for (int t = plo + tid; t < phi; t += kK8Threads)
+        if (prev[t] > prev[t + 1]) myd = t;
+      myd = __reduce_max_sync(0xffffffffu, myd);
+      if ((tid & 31) == 0 && myd >= 0) atomicMax(&s_dlast[j & 1], myd);
+      __syncthreads();
+      dl = s_dlast[j & 1];
+      if (tid == 0) s_dlast[(j + 1) & 1] = -1;          // for layer j+1 (read after its barrier)
+      if (dl >= 0) {
+        scan_prefix = dl - plo < a.vscan;
+        if (tid < 32) suffix_min_warp<T>(prev, plo, dl + 1, ssmd, tid);
+        if (!scan_prefix) {   // long descent prefix: masks + sparse table over its blocks
+          const int blo = plo >> 5, bhi = dl >> 5;
+          for (int blk = blo + (tid - 32); tid >= 32 && blk <= bhi; blk += kK8Threads - 32)
+            block_masks<T>(prev + (blk << 5), plo - (blk << 5), dl - (blk << 5), smask + (blk << 5), ssp + blk);
           __syncthreads();
+          for (int l = 1; (1 << l) <= bhi - blo + 1; ++l) {   // sparse levels over the block minima
+            const D* src = ssp + (int64_t)(l - 1) * nb;
+            D* dst = ssp + (int64_t)l * nb;
+            for (int blk = blo + tid; blk + (1 << l) - 1 <= bhi; blk += kK8Threads)
+              dst[blk] = T::vmin(src[blk], src[blk + (1 << (l - 1))]);
+            __syncthreads();
+          }
         }
+        __syncthreads();
       }
     }
     const int cap = scap[j - 1];
-    Valley<DT, KV, W> V{sL, RowMin<T>{prev, smask, ssp, ssp + nb, nb, mono},
+    Valley<DT, KV, W> V{sL, RowMin<T>{prev, ssmd, smask, ssp, ssp + nb, nb, dl},
                         gtab + (int64_t)srow[j - 1] * a.gstride, sSp, sWp,
-                        (cap >= 0 && cap < a.gstride - 1) ? cap : a.gstride - 1, KV ? skv[j - 1] : -1};
+                        (cap >= 0 && cap < a.gstride - 1) ? cap : a.gstride - 1, KV ? skv[j - 1] : -1,
+                        scan_prefix};
     if (j == 1) {   // dp[1][i] = L(tau_1) * T * F(i)
       for (int i = ilo + tid; i <= ihi; i += kK8Threads) {
         const D v = V.cost(0, i);
@@ -282,6 +346,8 @@ struct ValleyWs {                // K8L range-minimum workspace (per problem, ro
   uint32_t* mask;                // [2][B][nb*32]
   void* bm;                      // [2][B][nb]        block minima (sparse level 0)
   void* sp;                      // [B][levels-1][nb] sparse levels >= 1 (rebuilt per row)
+  void* smd;                     // [B][max_n+1]      suffix minima of the descent prefix (per row)
+  int* dlast;                    // [B]               last descent of the row (-1: none)
   int nbmax, lvmax;
 };
 
@@ -306,14 +372,16 @@ __global__ void __launch_bounds__(32 * kK8LWarps, 4) k8l_layer(SolveArgs a, int 
   for (int q = 0; q < a.D; ++q) row = (a.prof_deg[q] == d) ? q : row;
   const int cap = a.caps ? a.caps[(int64_t)b * a.cs + j - 1] : -1;
   const int pp = (j - 1) & 1;
-  const RowMin<T> rm{gdp + (int64_t)(j - 1) * (n + 1), w.mask + ((int64_t)pp * a.B + b) * nb * kVBlk,
+  const RowMin<T> rm{gdp + (int64_t)(j - 1) * (n + 1), reinterpret_cast<const D*>(w.smd) + (int64_t)b * (n + 1),
+                     w.mask + ((int64_t)pp * a.B + b) * nb * kVBlk,
                      reinterpret_cast<const D*>(w.bm) + ((int64_t)pp * a.B + b) * nb,
-                     reinterpret_cast<const D*>(w.sp) + (int64_t)b * (w.lvmax - 1) * nb, nb, false};
+                     reinterpret_cast<const D*>(w.sp) + (int64_t)b * (w.lvmax - 1) * nb, nb,
+                     j > 1 ? w.dlast[b] : -1};
   Valley<DT, KV, false> V{reinterpret_cast<const L*>(a.lengths) + (int64_t)b * a.ls, rm,
                           reinterpret_cast<const G*>(a.gtab) + (int64_t)row * a.gstride,
                           KV ? reinterpret_cast<const S*>(a.spws) + (int64_t)b * (n + 1) : nullptr, nullptr,
                           (cap >= 0 && cap < a.gstride - 1) ? cap : a.gstride - 1,
-                          KV ? a.kv[(int64_t)b * a.kvs + j - 1] : -1};
+                          KV ? a.kv[(int64_t)b * a.kvs + j - 1] : -1, false};
   const int x0 = (blk0 << 5) + kK8LRun * lane;
   int from = j - 1;
 #pragma unroll
@@ -345,21 +413,36 @@ __global__ void __launch_bounds__(32 * kK8LWarps, 4) k8l_layer(SolveArgs a, int 
   }
 }
 
-// sparse levels >= 1 over the block minima of row j (one CTA per problem)
+// Row j's range-minimum extras, after k8l_layer(j) (one CTA per problem): its last descent, the
+// suffix minima of the descent prefix, and sparse levels >= 1 over the prefix's block minima.
 template <int DT>
-__global__ void __launch_bounds__(1024) k8l_sparse(SolveArgs a, int j, ValleyWs w) {
+__global__ void __launch_bounds__(1024) k8l_rowprep(SolveArgs a, int j, ValleyWs w) {
   using T = Tr<DT, HEDDLE_MINMAX>;
   using D = typename T::D;
-  const int n = a.n, m = a.m, b = blockIdx.x;
+  __shared__ int s_dl;
+  const int n = a.n, m = a.m, b = blockIdx.x, tid = threadIdx.x;
   if (a.status[b] != HEDDLE_OK) return;
-  const int ilo = (j == 1) ? 1 : j, ihi = n - m + j;
-  const int blo = ilo >> 5, bhi = ihi >> 5, nb = vblocks(n);
+  const int ilo = (j == 1) ? 1 : j, ihi = n - m + j, nb = vblocks(n);
+  const D* row = reinterpret_cast<const D*>(a.dpws) + ((int64_t)b * (m + 1) + j) * (n + 1);
+  if (tid == 0) s_dl = -1;
+  __syncthreads();
+  int myd = -1;
+  for (int t = ilo + tid; t < ihi; t += blockDim.x)
+    if (row[t] > row[t + 1]) myd = t;
+  myd = __reduce_max_sync(0xffffffffu, myd);
+  if ((tid & 31) == 0 && myd >= 0) atomicMax(&s_dl, myd);
+  __syncthreads();
+  const int dl = s_dl;
+  if (tid == 0) w.dlast[b] = dl;
+  if (dl < 0) return;
+  if (tid < 32) suffix_min_warp<T>(row, ilo, dl + 1, reinterpret_cast<D*>(w.smd) + (int64_t)b * (n + 1), tid);
+  const int blo = ilo >> 5, bhi = dl >> 5;
   const D* bmj = reinterpret_cast<const D*>(w.bm) + ((int64_t)(j & 1) * a.B + b) * nb;
   D* sp = reinterpret_cast<D*>(w.sp) + (int64_t)b * (w.lvmax - 1) * nb;
   for (int l = 1; (1 << l) <= bhi - blo + 1; ++l) {
     const D* src = l == 1 ? bmj : sp + (int64_t)(l - 2) * nb;
     D* dst = sp + (int64_t)(l - 1) * nb;
-    for (int blk = blo + threadIdx.x; blk + (1 << l) - 1 <= bhi; blk += blockDim.x)
+    for (int blk = blo + tid; blk + (1 << l) - 1 <= bhi; blk += blockDim.x)
       dst[blk] = T::vmin(src[blk], src[blk + (1 << (l - 1))]);
     __syncthreads();
   }

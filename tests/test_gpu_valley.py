@@ -21,9 +21,17 @@ def _build():
     __graft_entry__.build()
 
 
+@pytest.fixture(params=["96", "0"], ids=["scan-prefix", "masks"])
+def vscan(request, monkeypatch):
+    """K8's two descent-prefix paths: scan the few states before the last descent (default), or
+    the masks + sparse-table range minimum (HEDDLE_PLACE_VALLEY_SCAN=0)."""
+    monkeypatch.setenv("HEDDLE_PLACE_VALLEY_SCAN", request.param)
+    return request.param
+
+
 @pytest.mark.parametrize("kernel", VALLEY_KERNELS)
 @pytest.mark.parametrize("dtype", ["u32", "f32"])
-def test_valley_random_tiny_exact(dtype, kernel):
+def test_valley_random_tiny_exact(dtype, kernel, vscan):
     """Heavy ties, clamp plateaus (flat F), caps, kv caps, heterogeneous degrees, infeasible and
     invalid problems: identical values, lowest-index boundaries and parent tables."""
     for s in range(200):
@@ -54,7 +62,7 @@ def test_valley_random_tiny_f64(kernel):
 
 
 @pytest.mark.parametrize("dtype", ["u32", "f32"])
-def test_valley_weighted_tiny_exact(dtype):
+def test_valley_weighted_tiny_exact(dtype, vscan):
     done = 0
     for s in range(200):
         batch = wl.tiny_random(s, n_max=20, m_max=6, allow_caps=True, allow_kv=True, allow_weights=True,
@@ -84,7 +92,7 @@ def test_valley_rollout_and_caps(kernel):
         assert_exact(gpu, 0, ref, batch, "f32", "minmax", check_parents=True, tag=f"valley-rollout{prob}")
 
 
-def test_valley_tp_sweep_and_batched_sample():
+def test_valley_tp_sweep_and_batched_sample(vscan):
     for batch, shared in ((wl.config_tp_sweep(), True), (wl.config_batched(B=96), False)):
         gpu = run_gpu(batch, lengths_shared=shared, algo="valley")
         rows = np.stack([batch.profile.row_of(batch.degrees[b]) for b in range(batch.B)])
@@ -109,7 +117,7 @@ def test_valley_medium_layered_vs_oracle():
     assert np.array_equal(gpu["bounds"], bounds)
 
 
-def test_valley_full_launches_equal_scan():
+def test_valley_full_launches_equal_scan(vscan):
     """The bench launches: all 16384 batched problems and the n = 65536, m = 256 instance --
     valley objectives and boundaries identical to the full scan's, problem by problem, and
     sampled batched problems identical to the oracle's."""
