@@ -205,19 +205,23 @@ int k2_smem(int dt, int sr, int n, int m, bool kv, bool w = false) {
 using K8Fn = void (*)(SolveArgs);
 using K8LFn = void (*)(SolveArgs, int, ValleyWs);
 using K8SFn = void (*)(SolveArgs, int, ValleyWs);
-template <int DT>
-K8Fn pick_k8(bool kp, bool kv, bool w) {
+template <int DT, int NT>
+K8Fn pick_k8n(bool kp, bool kv, bool w) {
   if (kp) {
-    if (w) return kv ? k8_valley<DT, true, true, true> : k8_valley<DT, true, false, true>;
-    return kv ? k8_valley<DT, true, true, false> : k8_valley<DT, true, false, false>;
+    if (w) return kv ? k8_valley<DT, true, true, true, NT> : k8_valley<DT, true, false, true, NT>;
+    return kv ? k8_valley<DT, true, true, false, NT> : k8_valley<DT, true, false, false, NT>;
   }
-  if (w) return kv ? k8_valley<DT, false, true, true> : k8_valley<DT, false, false, true>;
-  return kv ? k8_valley<DT, false, true, false> : k8_valley<DT, false, false, false>;
+  if (w) return kv ? k8_valley<DT, false, true, true, NT> : k8_valley<DT, false, false, true, NT>;
+  return kv ? k8_valley<DT, false, true, false, NT> : k8_valley<DT, false, false, false, NT>;
 }
-K8Fn k8_for(int dt, bool kp, bool kv, bool w) {
-  if (dt == HEDDLE_F32) return pick_k8<HEDDLE_F32>(kp, kv, w);
-  if (dt == HEDDLE_F64) return pick_k8<HEDDLE_F64>(kp, kv, w);
-  return pick_k8<HEDDLE_U32>(kp, kv, w);
+template <int DT>
+K8Fn pick_k8(bool kp, bool kv, bool w, bool wide) {
+  return wide ? pick_k8n<DT, kK8ThreadsWide>(kp, kv, w) : pick_k8n<DT, kK8Threads>(kp, kv, w);
+}
+K8Fn k8_for(int dt, bool kp, bool kv, bool w, bool wide) {
+  if (dt == HEDDLE_F32) return pick_k8<HEDDLE_F32>(kp, kv, w, wide);
+  if (dt == HEDDLE_F64) return pick_k8<HEDDLE_F64>(kp, kv, w, wide);
+  return pick_k8<HEDDLE_U32>(kp, kv, w, wide);
 }
 template <int DT>
 K8LFn pick_k8l(bool kp, bool kv) {
@@ -841,8 +845,8 @@ heddle_status heddle_place_init(const heddle_place_config* c, heddle_place_ctx**
     }
   if (c->flags & HEDDLE_VALLEY) {
     x->k8_smem_max = x->smem_optin;
-    for (int v = 0; v < 8; ++v) {
-      const void* fn = reinterpret_cast<const void*>(k8_for(x->dtype, v & 1, (v >> 1) & 1, v >> 2));
+    for (int v = 0; v < 16; ++v) {
+      const void* fn = reinterpret_cast<const void*>(k8_for(x->dtype, v & 1, (v >> 1) & 1, (v >> 2) & 1, v >> 3));
       cudaFuncAttributes fa{};
       if (cudaFuncGetAttributes(&fa, fn) != cudaSuccess ||
           cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -973,7 +977,8 @@ static heddle_status solve_impl(heddle_place_ctx* x, const heddle_place_problem*
     const heddle_status st = layered ? solve_valley_layered(x, a, kp, kv, s) : HEDDLE_OK;
     if (st != HEDDLE_OK) return st;
     if (!layered) {
-      k8_for(x->dtype, kp, kv, wt)<<<p->B, kK8Threads, smem2, s>>>(a);
+      const bool wide_cta = p->B < x->num_sms;
+      k8_for(x->dtype, kp, kv, wt, wide_cta)<<<p->B, wide_cta ? kK8ThreadsWide : kK8Threads, smem2, s>>>(a);
       x->launches++;
       if (cudaGetLastError() != cudaSuccess) return HEDDLE_E_CUDA;
     }

@@ -35,7 +35,10 @@
 
 namespace hp {
 
-constexpr int kK8Threads = 256;
+// K8 CTA sizes: 128 threads (8 CTAs, 32 warps per SM at <= 64 registers) when problems are
+// plentiful; 1024 threads when there are fewer problems than SMs (TP sweeps, single instances)
+constexpr int kK8Threads = 128;
+constexpr int kK8ThreadsWide = 1024;
 constexpr int kVBlk = 32;        // range-minimum block (one 32-bit mask per element)
 constexpr int kScanPrefix = 96;  // default SolveArgs::vscan: descent prefixes shorter than this are
                                  // scanned state by state (no masks / sparse table built)
@@ -128,11 +131,16 @@ struct Valley {
   const int* sWp;    // weight prefix sums (W)
   int ghi;           // largest admissible size (the worker's cap, else the table's end)
   int64_t kvc;       // token cap or < 0
-  bool scan_prefix;  // states i <= dlast+1 scan their splits (short descent prefix: no masks built)
+  bool scan_prefix;  // short descent prefix: no masks built (states i <= dlast+1 are scanned by the
+                     // caller; an argmin inside the prefix is found by walking it)
   // normalised cost of items [k, i) on worker j (+inf when inadmissible)
   __device__ __forceinline__ D cost(int k, int i) const {
     const int s = W ? sWp[i] - sWp[k] : i - k;
-    D v = T::norm(T::comb(T::zero(), sL[k], s <= ghi ? grow[s] : T::gpad()));
+    const G g = s <= ghi ? grow[s] : T::gpad();
+    D v;   // L * G in the DP kernels' rounding (Tr<>::comb with dp = 0; no max needed: L, G > 0)
+    if constexpr (DT == HEDDLE_F32) v = __fmul_rn(sL[k], g);
+    else if constexpr (DT == HEDDLE_F64) v = __dmul_rn(sL[k], g);
+    else v = T::norm(sL[k] * g);
     if constexpr (KV) {
       if (kvc >= 0 && sSp[i] - sSp[k] > (S)kvc) v = T::inf();
     }
@@ -143,33 +151,34 @@ struct Valley {
   template <bool ARG>
   __device__ __forceinline__ D solve(int lo, int i, int from, int& arg, int& kstar) const {
     const int hi = i - 1;
-    if (scan_prefix && hi <= rm.dlast) {   // Eq. 3 as written, lowest argmin (strict '<', k ascending)
-      D v = T::inf();
-      int bk = -1;
-      for (int k = lo; k <= hi; ++k) {
-        const D cv = cost(k, i), pv = rm.v[k];
-        const D c = pv > cv ? pv : cv;
-        if (c < v) { v = c; bk = k; }
-      }
-      if constexpr (ARG) arg = (v == T::inf()) ? -1 : bk;
-      kstar = lo;   // no crossing information: the next state searches from lo
-      return v;
-    }
-    auto crossed = [&](int k) { return rm(k, hi) >= cost(k, i); };
+    // the probes' values are kept: the answer min(rm(k*, hi), cost(k*-1, i)) is usually probed
+    D rm_t = T::inf(), c_f = T::inf();
+    bool have_cf = false;
+    auto crossed = [&](int k) {
+      const D r = rm(k, hi), c = cost(k, i);
+      if (r >= c) { rm_t = r; return true; }
+      c_f = c;
+      return false;
+    };
     int f = max(lo, from) - 1;   // last split known not crossed (or lo - 1)
     int t = hi + 1;              // first split known crossed (or hi + 1)
-    int step = 1;
-    for (int p = f + 1; p <= hi; p = f + step, step <<= 1) {   // gallop from `from`
-      if (crossed(p)) { t = p; break; }
-      f = p;
-    }
+    if (from > lo) {             // gallop from the previous state's crossing (usually 0-2 away)
+      int step = 1;
+      for (int p = f + 1; p <= hi; p = f + step, step <<= 1) {
+        if (crossed(p)) { t = p; break; }
+        f = p;
+        have_cf = true;
+      }
+    }                            // else: plain bisection of [lo, hi]
+    bool have_rt = t <= hi;
     while (t - f > 1) {
       const int mid = (f + t) >> 1;
-      if (crossed(mid)) t = mid; else f = mid;
+      if (crossed(mid)) { t = mid; have_rt = true; } else { f = mid; have_cf = true; }
     }
     kstar = t;
-    D v = (t <= hi) ? rm(t, hi) : T::inf();
-    if (t > lo) v = T::vmin(v, cost(t - 1, i));
+    // rm_t / c_f hold the last crossed / not-crossed probe, which are t and f when probed
+    D v = (t <= hi) ? (have_rt ? rm_t : rm(t, hi)) : T::inf();
+    if (t > lo) v = T::vmin(v, have_cf && f == t - 1 ? c_f : cost(t - 1, i));
     if constexpr (ARG) {
       if (v == T::inf()) {
         arg = -1;
@@ -203,12 +212,13 @@ struct Valley {
 template <int DT>
 struct K8Smem {
   using T = Tr<DT, HEDDLE_MINMAX>;
-  int lOff, d0Off, d1Off, smdOff, maskOff, spOff, sspOff, wpOff, rowOff, capOff, kvOff, total;
+  int lOff, gOff, d0Off, d1Off, smdOff, maskOff, spOff, sspOff, wpOff, rowOff, capOff, kvOff, total;
   __host__ __device__ K8Smem(int n, int m, bool kv, bool w) {
     int o = 0;
     auto take = [&](int bytes) { int at = o; o += (bytes + 15) & ~15; return at; };
     const int nb = vblocks(n);
     lOff = take((int)sizeof(typename T::L) * align4(n + kLPad));
+    gOff = w ? -1 : take((int)sizeof(typename T::G) * (n + 1));   // worker's cost row, cap-masked
     d0Off = take((int)sizeof(typename T::D) * nb * kVBlk);
     d1Off = take((int)sizeof(typename T::D) * nb * kVBlk);
     smdOff = take((int)sizeof(typename T::D) * (n + 1));
@@ -224,8 +234,8 @@ struct K8Smem {
 };
 
 // ---------------------------------------------------------------------------- K8: one CTA per problem
-template <int DT, bool KP, bool KV, bool W>
-__global__ void __launch_bounds__(kK8Threads, 4) k8_valley(SolveArgs a) {
+template <int DT, bool KP, bool KV, bool W, int NT>
+__global__ void __launch_bounds__(NT, 1024 / NT) k8_valley(SolveArgs a) {
   using T = Tr<DT, HEDDLE_MINMAX>;
   using L = typename T::L;
   using G = typename T::G;
@@ -235,6 +245,7 @@ __global__ void __launch_bounds__(kK8Threads, 4) k8_valley(SolveArgs a) {
   const int n = a.n, m = a.m, b = blockIdx.x, tid = threadIdx.x;
   const K8Smem<DT> lay(n, m, KV, W);
   L* sL = reinterpret_cast<L*>(smem + lay.lOff);
+  G* sG = W ? nullptr : reinterpret_cast<G*>(smem + lay.gOff);
   D* const sdp0 = reinterpret_cast<D*>(smem + lay.d0Off);
   D* const sdp1 = reinterpret_cast<D*>(smem + lay.d1Off);
   D* ssmd = reinterpret_cast<D*>(smem + lay.smdOff);
@@ -247,7 +258,7 @@ __global__ void __launch_bounds__(kK8Threads, 4) k8_valley(SolveArgs a) {
   int64_t* skv = reinterpret_cast<int64_t*>(smem + lay.kvOff);
   __shared__ int s_err, s_dlast[2];
   if (tid == 0) { s_dlast[0] = -1; s_dlast[1] = -1; }
-  if (load_problem<DT, HEDDLE_MINMAX, KV, W, kK8Threads>(a, b, sL, srow, scap, skv, sSp, sWp, s_err) != 0) return;
+  if (load_problem<DT, HEDDLE_MINMAX, KV, W, NT>(a, b, sL, srow, scap, skv, sSp, sWp, s_err) != 0) return;
   __syncthreads();
   D* gdp = reinterpret_cast<D*>(a.dpws) + (int64_t)b * (m + 1) * (n + 1);
   int32_t* gpar = KP ? a.parws + (int64_t)b * (m + 1) * (n + 1) : nullptr;
@@ -261,11 +272,20 @@ __global__ void __launch_bounds__(kK8Threads, 4) k8_valley(SolveArgs a) {
     const int ihi = (j == 1 || j < m) ? n - m + j : n;   // m == 1: layer 1 is the last (i up to n)
     int dl = -1;            // last descent of row j-1 (-1: non-decreasing)
     bool scan_prefix = false;
+    // worker j's cost row, masked by its cap (restaged only when the profile row or cap changes;
+    // the previous layer's reads ended at its last barrier)
+    const bool restage = !W && (j == 1 || srow[j - 1] != srow[j - 2] || scap[j - 1] != scap[j - 2]);
+    if (restage) {
+      const G* grow = gtab + (int64_t)srow[j - 1] * a.gstride;
+      const int cap = scap[j - 1], hi = (cap >= 0 && cap < n) ? cap : n;
+      for (int t = tid; t <= n; t += NT) sG[t] = (t >= 1 && t <= hi) ? grow[t] : T::gpad();
+    }
+    if (j == 1 && restage) __syncthreads();
     if (j > 1) {
       // range minimum of row j-1 over its computed region [j-1, n-m+j-1]
       const int plo = j - 1, phi = n - m + j - 1;
       int myd = -1;
-      for (int t = plo + tid; t < phi; t += kK8Threads)
+      for (int t = plo + tid; t < phi; t += NT)
         if (prev[t] > prev[t + 1]) myd = t;
       myd = __reduce_max_sync(0xffffffffu, myd);
       if ((tid & 31) == 0 && myd >= 0) atomicMax(&s_dlast[j & 1], myd);
@@ -277,13 +297,13 @@ __global__ void __launch_bounds__(kK8Threads, 4) k8_valley(SolveArgs a) {
         if (tid < 32) suffix_min_warp<T>(prev, plo, dl + 1, ssmd, tid);
         if (!scan_prefix) {   // long descent prefix: masks + sparse table over its blocks
           const int blo = plo >> 5, bhi = dl >> 5;
-          for (int blk = blo + (tid - 32); tid >= 32 && blk <= bhi; blk += kK8Threads - 32)
+          for (int blk = blo + (tid - 32); tid >= 32 && blk <= bhi; blk += NT - 32)
             block_masks<T>(prev + (blk << 5), plo - (blk << 5), dl - (blk << 5), smask + (blk << 5), ssp + blk);
           __syncthreads();
           for (int l = 1; (1 << l) <= bhi - blo + 1; ++l) {   // sparse levels over the block minima
             const D* src = ssp + (int64_t)(l - 1) * nb;
             D* dst = ssp + (int64_t)l * nb;
-            for (int blk = blo + tid; blk + (1 << l) - 1 <= bhi; blk += kK8Threads)
+            for (int blk = blo + tid; blk + (1 << l) - 1 <= bhi; blk += NT)
               dst[blk] = T::vmin(src[blk], src[blk + (1 << (l - 1))]);
             __syncthreads();
           }
@@ -293,20 +313,44 @@ __global__ void __launch_bounds__(kK8Threads, 4) k8_valley(SolveArgs a) {
     }
     const int cap = scap[j - 1];
     Valley<DT, KV, W> V{sL, RowMin<T>{prev, ssmd, smask, ssp, ssp + nb, nb, dl},
-                        gtab + (int64_t)srow[j - 1] * a.gstride, sSp, sWp,
-                        (cap >= 0 && cap < a.gstride - 1) ? cap : a.gstride - 1, KV ? skv[j - 1] : -1,
+                        W ? gtab + (int64_t)srow[j - 1] * a.gstride : sG, sSp, sWp,
+                        W ? ((cap >= 0 && cap < a.gstride - 1) ? cap : a.gstride - 1) : n, KV ? skv[j - 1] : -1,
                         scan_prefix};
     if (j == 1) {   // dp[1][i] = L(tau_1) * T * F(i)
-      for (int i = ilo + tid; i <= ihi; i += kK8Threads) {
+      for (int i = ilo + tid; i <= ihi; i += NT) {
         const D v = V.cost(0, i);
         cur[i] = v;
         if (KP) gpar[(int64_t)(n + 1) + i] = (v == T::inf()) ? -1 : 0;
       }
     } else {
-      // contiguous runs of states per thread, so each search gallops from the previous k*
-      const int ns = ihi - ilo + 1;
-      const int per = (ns + kK8Threads - 1) / kK8Threads;
-      const int r0 = ilo + tid * per, r1 = min(ihi, r0 + per - 1);
+      // states before the end of a short descent prefix (i - 1 <= dl): Eq. 3 as written, each by
+      // one warp (lanes over the splits, lowest-index argmin), dealt round-robin over the warps
+      const int pre_hi = scan_prefix ? min(dl + 1, ihi) : ilo - 1;
+      const int lane = tid & 31;
+      for (int i = ilo + (tid >> 5); i <= pre_hi; i += NT / 32) {
+        D best = T::inf();
+        int bk = INT_MAX;
+        for (int k = j - 1 + lane; k < i; k += 32) {
+          const D cv = V.cost(k, i), pv = prev[k];
+          const D c = pv > cv ? pv : cv;
+          if (c < best) { best = c; bk = k; }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          const D ov = shfl_down(best, off);
+          const int ok = __shfl_down_sync(0xffffffffu, bk, off);
+          if (ov < best || (ov == best && ok < bk)) { best = ov; bk = ok; }
+        }
+        if (lane == 0) {
+          cur[i] = best;
+          if (KP) gpar[(int64_t)j * (n + 1) + i] = (best == T::inf()) ? -1 : bk;
+        }
+      }
+      // the other states: contiguous runs per thread, so each search gallops from the previous k*
+      const int s0 = pre_hi + 1;
+      const int ns = ihi - s0 + 1;
+      const int per = (ns + NT - 1) / NT;
+      const int r0 = s0 + tid * per, r1 = min(ihi, r0 + per - 1);
       int from = j - 1;
       for (int i = r0; i <= r1; ++i) {
         int arg = -1, ks;
@@ -318,7 +362,7 @@ __global__ void __launch_bounds__(kK8Threads, 4) k8_valley(SolveArgs a) {
     }
     __syncthreads();
     // the finished row to the workspace (coalesced) for the backtrack; -1 parents off the region
-    for (int i = tid; i <= n; i += kK8Threads) {
+    for (int i = tid; i <= n; i += NT) {
       const bool in = (i >= ilo && i <= ihi);
       if (in) gdp[(int64_t)j * (n + 1) + i] = cur[i];
       if (KP && !in) gpar[(int64_t)j * (n + 1) + i] = -1;
