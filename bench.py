@@ -268,7 +268,31 @@ def run_cuda(args):
     torch.cuda.synchronize()
     t_e2e = e0.elapsed_time(e1) / 1e3
 
-    vals = torch.tensor([t_step, t_k2, t_e2e, float(launches)], dtype=torch.float64, device=dev)
+    # the same workload by the valley solver (HEDDLE_VALLEY): exact, O(n m log n);
+    # reported beside the scan (the metric's kernel), checked identical to it on this rank's problems
+    t_valley, same = -1.0, True
+    if args.valley and not (args.workload == "large" and world > 1):
+        obj_s, _ = placer.solve(L, D)
+        bnd_s = placer.backtrack()
+        vplacer = Placer.from_profile(batch.profile, max_n=n_, max_m=m_, max_batch=Bl, device=local, algo="valley")
+        for _ in range(2):
+            vplacer.solve(L, D)
+            vplacer.backtrack()
+        torch.cuda.synchronize()
+        evv = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
+        for s in range(args.steps):
+            flush.fill_(float(s))
+            evv[s][0].record(stream)
+            obj_v, _ = vplacer.solve(L, D)
+            bnd_v = vplacer.backtrack()
+            evv[s][1].record(stream)
+        torch.cuda.synchronize()
+        t_valley = sum(e[0].elapsed_time(e[1]) for e in evv) / 1e3
+        same = bool(torch.equal(obj_s, obj_v) and torch.equal(bnd_s, bnd_v))
+        vplacer.close()
+
+    vals = torch.tensor([t_step, t_k2, t_e2e, float(launches), t_valley, 0.0 if same else 1.0],
+                        dtype=torch.float64, device=dev)
     if world > 1:
         mx = vals.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
@@ -276,6 +300,7 @@ def run_cuda(args):
         dist.all_reduce(sm, op=dist.ReduceOp.SUM)
         t_step, t_k2, t_e2e = mx[0].item(), mx[1].item(), mx[2].item()
         launches = int(sm[3].item())
+        t_valley, same = mx[4].item(), mx[5].item() == 0.0
     cells = b_total * W * args.steps
     if rank == 0:
         value = cells / t_step
@@ -306,6 +331,13 @@ def run_cuda(args):
             "gpu_launches": launches,
             "clocks": clocks,
         }
+        if t_valley > 0:
+            line["valley"] = {
+                "what": "same workload and result by the exact valley search (HEDDLE_VALLEY, SURVEY 8f N3), "
+                        "solve + backtrack, device-resident; not the metric's kernel",
+                "ms_per_step": 1e3 * t_valley / args.steps, "solves_per_s": b_total * args.steps / t_valley,
+                "dp_equivalent_cells_per_s": cells / t_valley, "speedup_vs_scan": t_step / t_valley,
+                "identical_to_scan": same}
         if not args.no_cpu_baseline and world == 1 and args.workload == "batched":
             line["cpu_baseline"] = cpu_baseline(args.cpu_sample)
         print(json.dumps(line), flush=True)
@@ -323,6 +355,8 @@ def main():
     ap.add_argument("--workload", default="batched", choices=["batched", "large"],
                     help="batched = configs[3] (the metric's batched sweep, default); large = configs[4] split")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-valley", dest="valley", action="store_false",
+                    help="skip the valley-solver line (HEDDLE_VALLEY) reported beside the scan")
     ap.add_argument("--cpu-sample", type=int, default=2048)
     ap.add_argument("--ref-sample", type=int, default=32)
     ap.add_argument("--traffic", type=float, default=None, help="ncu dram bytes per K2 launch (from profiles/)")

@@ -5,7 +5,7 @@
 # 3) one --set full capture of k2_dp_batched.
 set -e
 TAG=${1:-r01}
-CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline"
+CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-valley"
 mkdir -p gpurun_out
 $CMD > gpurun_out/${TAG}_plain.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv \

@@ -137,10 +137,13 @@ class SAResult:
 class ResourceManager:
     """Batched-GPU evaluator for the SA walk.  One Placer (max_batch = chains)."""
 
-    def __init__(self, profile, n_max, m_max, chains, device=None, objective_only=False):
+    def __init__(self, profile, n_max, m_max, chains, device=None, objective_only=False, algo="valley"):
         """objective_only: evaluate makespans with the exact parametric kernel (heddle_place_objective,
-        N3) instead of the full DP; the best allocation's partition is solved by the DP at the end."""
-        self.placer = Placer.from_profile(profile, max_n=n_max, max_m=m_max, max_batch=chains, device=device)
+        N3) instead of the full DP; the best allocation's partition is solved by the DP at the end.
+        algo: the DP's solver, "valley" (N3, exact, O(n m log n)) or "scan" (every split of Eq. 3);
+        both give identical makespans and partitions."""
+        self.placer = Placer.from_profile(profile, max_n=n_max, max_m=m_max, max_batch=chains, device=device,
+                                          algo=algo)
         self.dev = self.placer.device
         self.evaluations = 0
         self.objective_only = objective_only

@@ -387,6 +387,11 @@ def test_sa_gpu_matches_oracle_sa():
     res2 = rm2.anneal(L, cfg, iu, su)
     assert res2.best_makespan == c and res2.best_degrees == N and res2.trace == res.trace
     assert np.array_equal(res2.best_boundaries, ref["bounds"])
+    # and with the full scan as the DP solver (the default is the valley search)
+    rm3 = alloc.ResourceManager(prof, n_max=256, m_max=40, chains=6, algo="scan")
+    res3 = rm3.anneal(L, cfg, iu, su)
+    assert res3.best_makespan == c and res3.best_degrees == N and res3.trace == res.trace
+    assert np.array_equal(res3.best_boundaries, ref["bounds"])
 
 
 @pytest.mark.parametrize("kernel", ["layered", "batched", "auto"])
