@@ -36,7 +36,7 @@ WORKLOAD = ("batched sweep (BASELINE configs[3]): 16384 independent N=1024 K=32 
             "coding(Pareto)/search(log-normal) families alternating, predicted FP32 lengths, random sorted "
             "MP degrees over {1,2,4,8}, Eq. 3 min-max")
 SM_COUNT = 148
-ISSUE_SLOTS_PER_CELL = 3   # FMUL + FMNMX(max) + FMNMX(min); measured issue rates in profiles/r01_alu_peaks.jsonl
+ISSUE_SLOTS_PER_CELL = 3   # ALU cycles per warp-transition: FMNMX (2) + half an FMNMX3 (1); profiles/r01_alu_peaks.jsonl
 
 
 def peaks():
@@ -62,8 +62,10 @@ def ncu_traffic(workload):
 
 
 def alu_peak_cells(sm_mhz):
-    """Issue-bound peak of the exhaustive Eq. 3 reduction: 4 SMSPs x 1 warp-instr/clk x 32 lanes
-    / 3 instructions per transition, x 148 SMs x clock."""
+    """ALU-pipe peak of the exhaustive Eq. 3 reduction: per SMSP the ALU pipe takes 2 cycles per
+    FMNMX / FMNMX3 warp instruction, and a transition needs one FMNMX (max) and half an FMNMX3
+    (min), i.e. 3 ALU cycles per warp-transition: 4 SMSPs x 32 lanes / 3 x 148 SMs x clock
+    (profiles/r01_alu_peaks.jsonl)."""
     return SM_COUNT * 4 * 32 / ISSUE_SLOTS_PER_CELL * sm_mhz * 1e6
 
 
@@ -201,14 +203,19 @@ def run_cuda(args):
         n_, m_, b_total, workload = N, M, B_TOTAL, WORKLOAD
         parallelism = f"dp{world} (problems block-sharded, no collective)"
         kernel_name = "k2_dp_batched<F32,MINMAX>"
-    else:   # configs[4]: one n=65536, m=256 instance, columns split across ranks (NCCL all-gather per layer)
+    else:   # configs[4]: one n=65536, m=256 instance, columns split across ranks (one row exchange per layer)
         batch = wl.config_large()
         lo, hi = 0, 1
         n_, m_, b_total = batch.n, batch.m, 1
         workload = ("single large instance (BASELINE configs[4]): N=65536 coding-like predicted lengths into "
                     "K=256 workers, FP32, Eq. 3 min-max")
-        parallelism = f"split{world} (zigzag column blocks, per-layer NCCL all-gather of the dp row)"
-        kernel_name = "k3_layer<F32,MINMAX>"
+        if os.environ.get("HEDDLE_PLACE_EXCHANGE", "") == "nccl":
+            parallelism = f"split{world} (zigzag 512-column blocks, per-layer NCCL all-gather of the dp row)"
+            kernel_name = "k3_layer<F32,MINMAX>"
+        else:
+            parallelism = (f"split{world} (zigzag 512-column blocks; fused exchange: the tile finishing a block "
+                           "stores it into every peer's dp row over NVLink peer memory)")
+            kernel_name = "k5_persistent<F32,MINMAX>"
     Bl = hi - lo
     L = torch.from_numpy(np.ascontiguousarray(batch.lengths[lo:hi])).to(dev)
     D = torch.from_numpy(np.ascontiguousarray(batch.degrees[lo:hi].astype(np.int32))).to(dev)
@@ -323,8 +330,8 @@ def run_cuda(args):
                          "traffic": args.traffic if args.traffic is not None else ncu_traffic(args.workload),
                          "algorithmic_bytes": (4 * n_ + 4 * m_ + 4 + 4 * (m_ + 1)) * (Bl if args.workload == "batched" else 1),
                          "kernel": kernel_name,
-                         "peak_basis": f"148 SMs x 4 SMSP x 32 lanes / 3 issue slots per cell x {peak_mhz:.0f} MHz "
-                                       "(measured issue rates, profiles/r01_alu_peaks.jsonl)",
+                         "peak_basis": f"148 SMs x 4 SMSP x 32 lanes / 3 ALU-pipe cycles per cell x {peak_mhz:.0f} MHz "
+                                       "(measured pipe rates, profiles/r01_alu_peaks.jsonl)",
                          "kernel_share_of_step": t_k2 / t_step},
             "e2e": {"value": cells / t_e2e, "unit": "cells/s", "h2d_bytes_per_step": h2d * world,
                     "d2h_bytes_per_step": d2h * world},

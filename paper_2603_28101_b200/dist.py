@@ -4,9 +4,11 @@
   (SURVEY §8e): the B problems are block-sharded across ranks; each rank solves and
   backtracks its shard on its own GPU with no collective on the data path.  The
   optional result gather at the end is one all_gather per output.
-* Split mode (one large instance): see `split_solve` -- the columns of every DP
-  layer are divided among the ranks and each finished row is all-gathered over
-  NCCL (inside libheddle_place.so).
+* Split mode (one large instance): see `split_placer` -- the columns of every DP
+  layer are dealt to the ranks in zigzag 512-column blocks.  Inside libheddle_place.so
+  the tile that finishes a block stores it into every peer's dp row over NVLink peer
+  memory (CUDA IPC) and bumps the peers' arrival counters (fused exchange, DESIGN.md §7);
+  HEDDLE_PLACE_EXCHANGE=nccl selects one NCCL all-gather of the row per layer instead.
 """
 from __future__ import annotations
 
