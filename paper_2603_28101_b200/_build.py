@@ -38,8 +38,8 @@ def sources():
 
 
 def deps():
-    return sources() + sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + [os.path.join(INCLUDE, "heddle_place.h"),
-                                                                         __file__]
+    return (sources() + sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + sorted(glob.glob(os.path.join(CSRC, "*.h")))
+            + [os.path.join(INCLUDE, "heddle_place.h"), __file__])
 
 
 STAMP = LIB + ".stamp"
@@ -62,9 +62,25 @@ def stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every translation unit (heddle_place.cu and the inst_*.cu kernel families) in
+    parallel, then link the shared library."""
     if not force and not stale():
         return LIB
-    cmd = [NVCC, *ARCH, *FLAGS, "-I", INCLUDE, "-shared", "-o", LIB, *sources(), *NCCL_FLAGS]
+    objdir = os.path.join(PKG, "build")
+    os.makedirs(objdir, exist_ok=True)
+    inc = ["-I", INCLUDE, "-I", os.path.join(NCCL, "include")]
+    procs, objs = [], []
+    for src in sources():
+        obj = os.path.join(objdir, os.path.splitext(os.path.basename(src))[0] + ".o")
+        cmd = [NVCC, *ARCH, *FLAGS, *inc, "-c", src, "-o", obj]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        procs.append((subprocess.Popen(cmd), cmd))
+        objs.append(obj)
+    failed = [cmd for p, cmd in procs if p.wait() != 0]
+    if failed:
+        raise subprocess.CalledProcessError(1, failed[0])
+    cmd = [NVCC, *ARCH, "-shared", "-cudart", "shared", "-o", LIB, *objs, *NCCL_FLAGS]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
@@ -74,12 +90,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 def build_checked(out: str) -> str:
-    """Debug build with shared-memory bounds checks (-DHEDDLE_CHECK_BOUNDS)."""
-    cmd = [NVCC, *ARCH, *FLAGS, "-DHEDDLE_CHECK_BOUNDS", "-I", INCLUDE, "-shared", "-o", out, *sources(), *NCCL_FLAGS]
+    """Debug build with shared-memory bounds checks (-DHEDDLE_CHECK_BOUNDS), one translation unit
+    (-DHEDDLE_UNITY) so that every kernel counts into the same device-side violation counter."""
+    cmd = [NVCC, *ARCH, *FLAGS, "-DHEDDLE_CHECK_BOUNDS", "-DHEDDLE_UNITY", "-I", INCLUDE, "-shared", "-o", out,
+           os.path.join(CSRC, "heddle_place.cu"), *NCCL_FLAGS]
     subprocess.check_call(cmd)
     return out
-
-
-if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
-    print(LIB)

@@ -1,0 +1,40 @@
+// Kernel dispatch tables shared by the host code (heddle_place.cu) and the translation units
+// that instantiate the large kernel families (inst_*.cu, compiled in parallel; a -DHEDDLE_UNITY
+// build includes them into heddle_place.cu instead).  Each getter returns the kernel variant for a
+// dtype / semiring / feature combination; the launch stays in heddle_place.cu.
+#pragma once
+#include <cstdint>
+
+#include "backtrack.cuh"
+#include "dp_batched.cuh"
+#include "dp_layered.cuh"
+#include "heddle_place.h"
+#include "valley.cuh"
+
+using K2Fn = void (*)(hp::SolveArgs);
+using K4Fn = void (*)(hp::SolveArgs, int32_t*);
+using K3Fn = void (*)(hp::LayerArgs);
+using K5Fn = void (*)(hp::PersistArgs);
+using KPro = void (*)(hp::SolveArgs);
+using K8Fn = void (*)(hp::SolveArgs);
+using K8LFn = void (*)(hp::SolveArgs, int, hp::ValleyWs);
+using K8SFn = void (*)(hp::SolveArgs, int, hp::ValleyWs);
+
+// dt: heddle_dtype, sr: heddle_semiring
+#define HP_DISPATCH(NAME, ...)                                                                          \
+  (dt == HEDDLE_F32 ? (sr == HEDDLE_MINMAX ? NAME<HEDDLE_F32, HEDDLE_MINMAX>(__VA_ARGS__)               \
+                                           : NAME<HEDDLE_F32, HEDDLE_MINPLUS>(__VA_ARGS__))             \
+   : dt == HEDDLE_F64 ? (sr == HEDDLE_MINMAX ? NAME<HEDDLE_F64, HEDDLE_MINMAX>(__VA_ARGS__)             \
+                                             : NAME<HEDDLE_F64, HEDDLE_MINPLUS>(__VA_ARGS__))           \
+                      : (sr == HEDDLE_MINMAX ? NAME<HEDDLE_U32, HEDDLE_MINMAX>(__VA_ARGS__)             \
+                                             : NAME<HEDDLE_U32, HEDDLE_MINPLUS>(__VA_ARGS__)))
+
+K2Fn k2_for(int dt, int sr, bool kp, bool kv, bool w = false);   // inst_k2.cu
+K4Fn k4_for(int dt, int sr, bool kv, bool w);                     // inst_k4.cu
+K4Fn k4c_for(int dt, int sr, bool kv, bool w);
+K3Fn k3_for(int dt, int sr, bool kp, bool kv);                    // inst_k35.cu
+KPro pro_for(int dt, int sr, bool kp, bool kv);
+K5Fn k5_for(int dt, int sr);
+K8Fn k8_for(int dt, bool kp, bool kv, bool w, bool wide);         // inst_k8.cu
+K8LFn k8l_for(int dt, bool kp, bool kv);
+K8SFn k8lr_for(int dt);

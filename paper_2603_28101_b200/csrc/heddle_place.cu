@@ -17,6 +17,7 @@
 #include "backtrack.cuh"
 #include "dp_batched.cuh"
 #include "dp_layered.cuh"
+#include "dispatch.h"
 #include "heddle_place.h"
 #include "migration.cuh"
 #include "parametric.cuh"
@@ -135,63 +136,6 @@ struct DeviceGuard {
   }
 };
 
-using K2Fn = void (*)(SolveArgs);
-using K4Fn = void (*)(SolveArgs, int32_t*);
-
-template <int DT, int SR>
-K2Fn pick_k2(bool kp, bool kv, bool w) {
-  if (w) {
-    if (kp) return kv ? k2_dp_batched<DT, SR, true, true, true> : k2_dp_batched<DT, SR, true, false, true>;
-    return kv ? k2_dp_batched<DT, SR, false, true, true> : k2_dp_batched<DT, SR, false, false, true>;
-  }
-  if (kp) return kv ? k2_dp_batched<DT, SR, true, true> : k2_dp_batched<DT, SR, true, false>;
-  return kv ? k2_dp_batched<DT, SR, false, true> : k2_dp_batched<DT, SR, false, false>;
-}
-template <int DT, int SR>
-K4Fn pick_k4(bool kv, bool w) {
-  if (w) return kv ? k4_backtrack<DT, SR, true, true> : k4_backtrack<DT, SR, false, true>;
-  return kv ? k4_backtrack<DT, SR, true> : k4_backtrack<DT, SR, false>;
-}
-template <int DT, int SR>
-K4Fn pick_k4c(bool kv, bool w) {
-  if (w) return kv ? k4_backtrack_cta<DT, SR, true, true> : k4_backtrack_cta<DT, SR, false, true>;
-  return kv ? k4_backtrack_cta<DT, SR, true> : k4_backtrack_cta<DT, SR, false>;
-}
-
-K2Fn k2_for(int dt, int sr, bool kp, bool kv, bool w = false) {
-  if (dt == HEDDLE_F32) return sr == HEDDLE_MINMAX ? pick_k2<HEDDLE_F32, HEDDLE_MINMAX>(kp, kv, w) : pick_k2<HEDDLE_F32, HEDDLE_MINPLUS>(kp, kv, w);
-  if (dt == HEDDLE_F64) return sr == HEDDLE_MINMAX ? pick_k2<HEDDLE_F64, HEDDLE_MINMAX>(kp, kv, w) : pick_k2<HEDDLE_F64, HEDDLE_MINPLUS>(kp, kv, w);
-  return sr == HEDDLE_MINMAX ? pick_k2<HEDDLE_U32, HEDDLE_MINMAX>(kp, kv, w) : pick_k2<HEDDLE_U32, HEDDLE_MINPLUS>(kp, kv, w);
-}
-K4Fn k4_for(int dt, int sr, bool kv, bool w) {
-  if (dt == HEDDLE_F32) return sr == HEDDLE_MINMAX ? pick_k4<HEDDLE_F32, HEDDLE_MINMAX>(kv, w) : pick_k4<HEDDLE_F32, HEDDLE_MINPLUS>(kv, w);
-  if (dt == HEDDLE_F64) return sr == HEDDLE_MINMAX ? pick_k4<HEDDLE_F64, HEDDLE_MINMAX>(kv, w) : pick_k4<HEDDLE_F64, HEDDLE_MINPLUS>(kv, w);
-  return sr == HEDDLE_MINMAX ? pick_k4<HEDDLE_U32, HEDDLE_MINMAX>(kv, w) : pick_k4<HEDDLE_U32, HEDDLE_MINPLUS>(kv, w);
-}
-
-using K3Fn = void (*)(LayerArgs);
-using K5Fn = void (*)(PersistArgs);
-using KPro = void (*)(SolveArgs);
-template <int DT, int SR>
-K3Fn pick_k3(bool kp, bool kv) {
-  if (kp) return kv ? k3_layer<DT, SR, true, true> : k3_layer<DT, SR, true, false>;
-  return kv ? k3_layer<DT, SR, false, true> : k3_layer<DT, SR, false, false>;
-}
-template <int DT, int SR>
-KPro pick_pro(bool kp, bool kv) {
-  if (kp) return kv ? k3_prologue<DT, SR, true, true> : k3_prologue<DT, SR, true, false>;
-  return kv ? k3_prologue<DT, SR, false, true> : k3_prologue<DT, SR, false, false>;
-}
-#define HP_DISPATCH(NAME, ...)                                                                          \
-  (dt == HEDDLE_F32 ? (sr == HEDDLE_MINMAX ? NAME<HEDDLE_F32, HEDDLE_MINMAX>(__VA_ARGS__)               \
-                                           : NAME<HEDDLE_F32, HEDDLE_MINPLUS>(__VA_ARGS__))             \
-   : dt == HEDDLE_F64 ? (sr == HEDDLE_MINMAX ? NAME<HEDDLE_F64, HEDDLE_MINMAX>(__VA_ARGS__)             \
-                                             : NAME<HEDDLE_F64, HEDDLE_MINPLUS>(__VA_ARGS__))           \
-                      : (sr == HEDDLE_MINMAX ? NAME<HEDDLE_U32, HEDDLE_MINMAX>(__VA_ARGS__)             \
-                                             : NAME<HEDDLE_U32, HEDDLE_MINPLUS>(__VA_ARGS__)))
-K3Fn k3_for(int dt, int sr, bool kp, bool kv) { return HP_DISPATCH(pick_k3, kp, kv); }
-K4Fn k4c_for(int dt, int sr, bool kv, bool w) { return HP_DISPATCH(pick_k4c, kv, w); }
-KPro pro_for(int dt, int sr, bool kp, bool kv) { return HP_DISPATCH(pick_pro, kp, kv); }
 template <int DT, int SR> int k3_smem_t(int kc) { return K3Smem<DT, SR>(kc).total; }
 int k3_smem(int dt, int sr, int kc) { return HP_DISPATCH(k3_smem_t, kc); }
 
@@ -202,42 +146,6 @@ int k2_smem(int dt, int sr, int n, int m, bool kv, bool w = false) {
 }
 
 // K8 / K8L (valley solver, min-max only)
-using K8Fn = void (*)(SolveArgs);
-using K8LFn = void (*)(SolveArgs, int, ValleyWs);
-using K8SFn = void (*)(SolveArgs, int, ValleyWs);
-template <int DT, int NT>
-K8Fn pick_k8n(bool kp, bool kv, bool w) {
-  if (kp) {
-    if (w) return kv ? k8_valley<DT, true, true, true, NT> : k8_valley<DT, true, false, true, NT>;
-    return kv ? k8_valley<DT, true, true, false, NT> : k8_valley<DT, true, false, false, NT>;
-  }
-  if (w) return kv ? k8_valley<DT, false, true, true, NT> : k8_valley<DT, false, false, true, NT>;
-  return kv ? k8_valley<DT, false, true, false, NT> : k8_valley<DT, false, false, false, NT>;
-}
-template <int DT>
-K8Fn pick_k8(bool kp, bool kv, bool w, bool wide) {
-  return wide ? pick_k8n<DT, kK8ThreadsWide>(kp, kv, w) : pick_k8n<DT, kK8Threads>(kp, kv, w);
-}
-K8Fn k8_for(int dt, bool kp, bool kv, bool w, bool wide) {
-  if (dt == HEDDLE_F32) return pick_k8<HEDDLE_F32>(kp, kv, w, wide);
-  if (dt == HEDDLE_F64) return pick_k8<HEDDLE_F64>(kp, kv, w, wide);
-  return pick_k8<HEDDLE_U32>(kp, kv, w, wide);
-}
-template <int DT>
-K8LFn pick_k8l(bool kp, bool kv) {
-  if (kp) return kv ? k8l_layer<DT, true, true> : k8l_layer<DT, true, false>;
-  return kv ? k8l_layer<DT, false, true> : k8l_layer<DT, false, false>;
-}
-K8LFn k8l_for(int dt, bool kp, bool kv) {
-  if (dt == HEDDLE_F32) return pick_k8l<HEDDLE_F32>(kp, kv);
-  if (dt == HEDDLE_F64) return pick_k8l<HEDDLE_F64>(kp, kv);
-  return pick_k8l<HEDDLE_U32>(kp, kv);
-}
-K8SFn k8lr_for(int dt) {
-  if (dt == HEDDLE_F32) return k8l_rowprep<HEDDLE_F32>;
-  if (dt == HEDDLE_F64) return k8l_rowprep<HEDDLE_F64>;
-  return k8l_rowprep<HEDDLE_U32>;
-}
 int k8_smem(int dt, int n, int m, bool kv, bool w) {
   if (dt == HEDDLE_F32) return K8Smem<HEDDLE_F32>(n, m, kv, w).total;
   if (dt == HEDDLE_F64) return K8Smem<HEDDLE_F64>(n, m, kv, w).total;
@@ -333,9 +241,6 @@ bool per_problem_kernel(const heddle_place_ctx* x, int n, int m, int B, bool kv,
   if (x->flags & HEDDLE_FORCE_LAYERED) return false;
   return k2_smem(x->dtype, x->semiring, n, m, kv, wt) <= x->k2_smem_max && !use_layered(x, n, m, B);
 }
-
-template <int DT, int SR>
-K5Fn pick_k5() { return k5_persistent<DT, SR>; }
 
 // K5 (persistent dataflow over all layers); fill + prologue have been enqueued already.
 heddle_status solve_persistent(heddle_place_ctx* x, SolveArgs& a, cudaStream_t s) {
@@ -449,7 +354,7 @@ heddle_status solve_persistent(heddle_place_ctx* x, SolveArgs& a, cudaStream_t s
     pa.a.err = x->d_err;
     a.err = x->d_err;
   }
-  K5Fn fn = HP_DISPATCH(pick_k5);
+  K5Fn fn = k5_for(dt, sr);
   const int smem = k3_smem(dt, sr, kc);
   int occ = 0;
   cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1380,3 +1285,10 @@ heddle_status heddle_place_objective(heddle_place_ctx* x, const heddle_place_pro
 }
 
 }  // extern "C"
+
+#ifdef HEDDLE_UNITY   // debug / bounds-checked build: one translation unit
+#include "inst_k2.cu"
+#include "inst_k35.cu"
+#include "inst_k4.cu"
+#include "inst_k8.cu"
+#endif

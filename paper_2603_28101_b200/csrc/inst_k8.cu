@@ -1,0 +1,41 @@
+// K8 / K8L valley kernels (valley.cuh, min-max only).
+#ifndef HEDDLE_UNITY
+#define HEDDLE_INST_TU   // the non-template kernels live in heddle_place.cu's translation unit
+#endif
+#include "dispatch.h"
+
+using namespace hp;
+
+template <int DT, int NT>
+K8Fn pick_k8n(bool kp, bool kv, bool w) {
+  if (kp) {
+    if (w) return kv ? k8_valley<DT, true, true, true, NT> : k8_valley<DT, true, false, true, NT>;
+    return kv ? k8_valley<DT, true, true, false, NT> : k8_valley<DT, true, false, false, NT>;
+  }
+  if (w) return kv ? k8_valley<DT, false, true, true, NT> : k8_valley<DT, false, false, true, NT>;
+  return kv ? k8_valley<DT, false, true, false, NT> : k8_valley<DT, false, false, false, NT>;
+}
+template <int DT>
+K8Fn pick_k8(bool kp, bool kv, bool w, bool wide) {
+  return wide ? pick_k8n<DT, kK8ThreadsWide>(kp, kv, w) : pick_k8n<DT, kK8Threads>(kp, kv, w);
+}
+K8Fn k8_for(int dt, bool kp, bool kv, bool w, bool wide) {
+  if (dt == HEDDLE_F32) return pick_k8<HEDDLE_F32>(kp, kv, w, wide);
+  if (dt == HEDDLE_F64) return pick_k8<HEDDLE_F64>(kp, kv, w, wide);
+  return pick_k8<HEDDLE_U32>(kp, kv, w, wide);
+}
+template <int DT>
+K8LFn pick_k8l(bool kp, bool kv) {
+  if (kp) return kv ? k8l_layer<DT, true, true> : k8l_layer<DT, true, false>;
+  return kv ? k8l_layer<DT, false, true> : k8l_layer<DT, false, false>;
+}
+K8LFn k8l_for(int dt, bool kp, bool kv) {
+  if (dt == HEDDLE_F32) return pick_k8l<HEDDLE_F32>(kp, kv);
+  if (dt == HEDDLE_F64) return pick_k8l<HEDDLE_F64>(kp, kv);
+  return pick_k8l<HEDDLE_U32>(kp, kv);
+}
+K8SFn k8lr_for(int dt) {
+  if (dt == HEDDLE_F32) return k8l_rowprep<HEDDLE_F32>;
+  if (dt == HEDDLE_F64) return k8l_rowprep<HEDDLE_F64>;
+  return k8l_rowprep<HEDDLE_U32>;
+}
