@@ -492,7 +492,15 @@ struct PersistArgs {
   const unsigned long long* start_flag;    // split mode: solve-start barrier counter
   unsigned long long wait_start;
   int* err;
+  unsigned long long* trace;       // [tiles][4] %globaltimer: dequeued, dependencies met, staged, done
+                                   // (HEDDLE_PLACE_TILE_TRACE diagnostics), or null
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 template <int DT, int SR>
 __global__ void __launch_bounds__(kK3Threads) k5_persistent(PersistArgs pa) {
@@ -518,6 +526,8 @@ __global__ void __launch_bounds__(kK3Threads) k5_persistent(PersistArgs pa) {
     __syncthreads();
     const int64_t tile = s_tile;
     if (tile >= ntiles) break;
+    unsigned long long* tr = pa.trace ? pa.trace + 4 * tile : nullptr;
+    if (tr && tid == 0) tr[0] = gtimer();
     const int4 tl = pa.tiles[tile / B];
     const int b = (int)(tile % B);
     const int j = tl.x, blk = tl.y, q = tl.z, nch = tl.w;
@@ -544,6 +554,7 @@ __global__ void __launch_bounds__(kK3Threads) k5_persistent(PersistArgs pa) {
       __syncthreads();
       if (!s_flag) break;
     }
+    if (tr && tid == 0) tr[1] = gtimer();
     const L* gL = reinterpret_cast<const L*>(a.lengths) + (int64_t)b * a.ls;
     const D* gprev = reinterpret_cast<const D*>(a.dpws) + ((int64_t)b * (m + 1) + (j - 1)) * (n + 1);
     D* gcur = reinterpret_cast<D*>(a.dpws) + ((int64_t)b * (m + 1) + j) * (n + 1);
@@ -568,6 +579,7 @@ __global__ void __launch_bounds__(kK3Threads) k5_persistent(PersistArgs pa) {
       if (t > 0) sG2[t - 1] = g;
     }
     __syncthreads();
+    if (tr && tid == 0) tr[2] = gtimer();
     const int cw = c0 + kWarpCols * warp;
     if (cw <= imaxb) {
       const int c = cw + kLaneCols * cl;
@@ -626,6 +638,7 @@ __global__ void __launch_bounds__(kK3Threads) k5_persistent(PersistArgs pa) {
       }
       if (tid == 0) atomicAdd_system(pa.ready + bidx, 1ull);   // local consumers
     }
+    if (tr && tid == 0) tr[3] = gtimer();
     __syncthreads();
   }
 }

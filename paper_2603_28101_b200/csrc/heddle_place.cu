@@ -371,8 +371,31 @@ heddle_status solve_persistent(heddle_place_ctx* x, SolveArgs& a, cudaStream_t s
     for (auto& e : tev) cudaEventCreate(&e);
     cudaEventRecord(tev[0], s);
   }
+  // HEDDLE_PLACE_TILE_TRACE=<file>: append this solve's per-tile timeline (diagnostics only)
+  const char* ttrace = std::getenv("HEDDLE_PLACE_TILE_TRACE");
+  unsigned long long* d_trace = nullptr;
+  if (ttrace && ttrace[0]) {
+    if (cudaMalloc(&d_trace, 32 * (size_t)ntiles) != cudaSuccess) { cudaGetLastError(); d_trace = nullptr; }
+    else cudaMemsetAsync(d_trace, 0, 32 * (size_t)ntiles, s);
+    pa.trace = d_trace;
+  }
   fn<<<grid, kK3Threads, smem, s>>>(pa);
   x->launches++;
+  if (d_trace) {
+    std::vector<unsigned long long> h(4 * (size_t)ntiles);
+    std::vector<int4> tl(x->tiles_n);
+    cudaMemcpyAsync(h.data(), d_trace, 32 * (size_t)ntiles, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(tl.data(), x->d_tiles, sizeof(int4) * tl.size(), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    cudaFree(d_trace);
+    if (FILE* f = std::fopen(ttrace, "ab")) {   // record: int64 {ntiles, B, kc, grid, rank, world}, int4 tiles, u64 times
+      const int64_t hdr[6] = {ntiles, B, kc, grid, rank, world};
+      std::fwrite(hdr, sizeof(hdr), 1, f);
+      std::fwrite(tl.data(), sizeof(int4), tl.size(), f);
+      std::fwrite(h.data(), 8, h.size(), f);
+      std::fclose(f);
+    }
+  }
   if (world > 1) {
     k5_wait_arrivals<<<1, 1, 0, s>>>(pa);
     x->launches++;
