@@ -1,7 +1,8 @@
 """Summarise a K5 per-tile timeline written under HEDDLE_PLACE_TILE_TRACE=<file> (diagnostics).
 
-Each record: int64 {ntiles, B, kc, grid, rank, world}; int4 tiles[nentries] = {j, blk, q, nch};
-u64 times[ntiles][4] = %globaltimer (ns) at dequeue, dependencies met, staged, done.
+Each record: int64 {ntiles, B, kc, grid, rank, world}; int4 tiles[nentries] = {j, blk | nch << 16, k0, k1};
+u64 times[ntiles][6] = %globaltimer (ns) at: start (tile index known), L and G staged (thread 0's share),
+row j-1 dependencies met, dp staged, swept, published.
 Tile t is entry t // B of problem t % B.
 
     python bench/tile_trace.py <file> [--record -1]
@@ -23,10 +24,13 @@ def records(path):
         nent = int(ntiles) // int(B)
         tiles = np.frombuffer(raw, np.int32, 4 * nent, off).reshape(nent, 4)
         off += 16 * nent
-        t = np.frombuffer(raw, np.uint64, 4 * int(ntiles), off).reshape(int(ntiles), 4).astype(np.int64)
-        off += 32 * int(ntiles)
+        t = np.frombuffer(raw, np.uint64, 6 * int(ntiles), off).reshape(int(ntiles), 6).astype(np.int64)
+        off += 48 * int(ntiles)
         yield dict(ntiles=int(ntiles), B=int(B), kc=int(kc), grid=int(grid), rank=int(rank), world=int(world),
                    tiles=tiles, t=t)
+
+
+PHASES = ["stage L,G", "wait row j-1", "stage dp", "sweep", "publish"]
 
 
 def summarise(r):
@@ -34,34 +38,22 @@ def summarise(r):
     t = t - t[:, 0].min()
     ent = np.repeat(r["tiles"], r["B"], axis=0)
     j = ent[:, 0]
-    span = t[:, 3].max()
-    wait = (t[:, 1] - t[:, 0]).sum()
-    stage = (t[:, 2] - t[:, 1]).sum()
-    work = (t[:, 3] - t[:, 2]).sum()
+    span = t[:, 5].max()
     slots = r["grid"] * span
+    ph = np.diff(t, axis=1)                       # [tiles][5] phase durations
+    share = {p: float(ph[:, i].sum() / slots) for i, p in enumerate(PHASES)}
+    share["between tiles"] = 1.0 - sum(share.values())
     layers = np.unique(j)
-    done = np.array([t[j == k, 3].max() for k in layers])
-    first = np.array([t[j == k, 0].min() for k in layers])
+    done = np.array([t[j == k, 5].max() for k in layers])
     dj = np.diff(done)
-    # the tile whose completion ends each layer, and how long it waited / computed
-    last = [np.flatnonzero(j == k)[np.argmax(t[j == k, 3])] for k in layers]
-    lw = np.array([t[i, 1] - t[i, 0] for i in last])
-    ls = np.array([t[i, 2] - t[i, 1] for i in last])
-    lc = np.array([t[i, 3] - t[i, 2] for i in last])
     return {
         "tiles": r["ntiles"], "B": r["B"], "kc": r["kc"], "grid": r["grid"], "rank": r["rank"], "world": r["world"],
         "span_us": span / 1e3,
-        "cta_time_share": {"waiting": wait / slots, "staging": stage / slots, "sweep+publish": work / slots,
-                           "idle (no tile)": 1 - (wait + stage + work) / slots},
-        "tile_us_median": {"wait": float(np.median(t[:, 1] - t[:, 0]) / 1e3),
-                           "stage": float(np.median(t[:, 2] - t[:, 1]) / 1e3),
-                           "sweep+publish": float(np.median(t[:, 3] - t[:, 2]) / 1e3)},
+        "cta_time_share": share,
+        "tile_us_median": {p: float(np.median(ph[:, i]) / 1e3) for i, p in enumerate(PHASES)},
+        "tile_us_mean": {p: float(ph[:, i].mean() / 1e3) for i, p in enumerate(PHASES)},
         "layer_done_step_us": {"median": float(np.median(dj) / 1e3), "mean": float(dj.mean() / 1e3),
                                "max": float(dj.max() / 1e3)},
-        "layer_last_tile_us_median": {"wait": float(np.median(lw) / 1e3), "stage": float(np.median(ls) / 1e3),
-                                      "sweep+publish": float(np.median(lc) / 1e3)},
-        "layers_in_flight_median": float(np.median([(first <= x).sum() - (done < x).sum()
-                                                    for x in np.linspace(0, span, 200)])),
     }
 
 

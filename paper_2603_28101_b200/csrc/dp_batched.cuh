@@ -77,6 +77,7 @@ struct SolveArgs {
   unsigned ready_epoch;
   int ready_chunk;
   int vscan;               // valley kernel: descent prefixes shorter than this are scanned (K8)
+  int2* rowcap;            // [B][m] {profile row, cap} per worker, written by the K3/K5 prologue, or null
 };
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {

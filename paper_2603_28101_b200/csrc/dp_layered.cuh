@@ -138,6 +138,8 @@ __global__ void __launch_bounds__(256) k3_prologue(SolveArgs a) {
     for (int q = 0; q < a.D; ++q) row = (a.prof_deg[q] == d) ? q : row;
     if (row < 0) atomicMin(&s_err, (int)HEDDLE_E_UNKNOWN_DEGREE);
     if (j + 1 < m && a.degrees[(int64_t)b * a.ds + j + 1] > d) atomicMin(&s_err, (int)HEDDLE_E_UNSORTED);
+    if (a.rowcap)   // per-worker profile row and cap for K5's tiles (one load instead of three)
+      a.rowcap[(int64_t)b * m + j] = make_int2(row < 0 ? 0 : row, a.caps ? a.caps[(int64_t)b * a.cs + j] : -1);
   }
   __syncthreads();
   int err = s_err == INT_MAX ? 0 : s_err;
@@ -474,6 +476,26 @@ __global__ void __launch_bounds__(kK3Threads) k3_layer(LayerArgs la) {
 // and, in split mode, first stores the block's final values into every peer's dp row
 // over NVLink (CUDA-IPC peer memory) and bumps the peers' counters (system scope).
 // Deadlock freedom: every dependency of a tile was dequeued earlier, by a running CTA.
+// Cooperative staging global -> shared with U independent loads per thread in flight before the
+// stores (a plain loop issues one load, one store, one load ...: one L2 round trip per element
+// row per thread).  load(t) / store(t, v) for t in [0, cnt).
+template <int NT, int U, class LD, class ST>
+__device__ __forceinline__ void stage_batched(int cnt, LD&& load, ST&& store) {
+  for (int base = threadIdx.x; base < cnt; base += U * NT) {
+    decltype(load(0)) v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int t = base + u * NT;
+      if (t < cnt) v[u] = load(t);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int t = base + u * NT;
+      if (t < cnt) store(t, v[u]);
+    }
+  }
+}
+
 struct PersistArgs {
   SolveArgs a;
   int kc, ncb;
@@ -492,7 +514,12 @@ struct PersistArgs {
   const unsigned long long* start_flag;    // split mode: solve-start barrier counter
   unsigned long long wait_start;
   int* err;
-  unsigned long long* trace;       // [tiles][4] %globaltimer: dequeued, dependencies met, staged, done
+  const int* nch;                  // [m+1][ncb] chunks per column block (single-GPU ready target)
+  const void* gA;                  // cost table rows at stride gsp, row r at gA + r*gsp (16-B aligned at s == 1 mod 4)
+  const void* gB;                  // the same, 16-B aligned at s == 2 mod 4 (the one-element-shifted window)
+  int gsp;
+  unsigned long long* trace;       // [tiles][6] %globaltimer: start, L/G staged, dependencies met, dp staged,
+                                   // swept, published
                                    // (HEDDLE_PLACE_TILE_TRACE diagnostics), or null
 };
 
@@ -502,8 +529,63 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
+// ---- 1-D bulk copies (TMA engine, cp.async.bulk) into shared memory, completed on an mbarrier
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(unsigned long long* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
+  asm volatile("{\n\t.reg .pred p;\n"
+               "WAIT_%=:\n\t"
+               "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+               "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+// elements [t0, t1) of a staged window G(lo + t), t in [0, len), that one bulk copy from `src` (a
+// cost-table row, index s) can fill: s in [1, ghi], both ends on 16-byte boundaries; empty if the
+// source is not aligned there
+template <class G>
+__device__ __forceinline__ void bulk_span(const G* src, int lo, int len, int ghi, int& t0, int& t1) {
+  constexpr int E = 16 / (int)sizeof(G);
+  const int a = lo >= 1 ? lo : lo + ((1 - lo + E - 1) / E) * E;
+  const int e = min(lo + len, ghi + 1);
+  const int ee = e > a ? a + ((e - a) / E) * E : a;
+  if (ee <= a || (reinterpret_cast<uintptr_t>(src + a) & 15)) { t0 = t1 = 0; return; }
+  t0 = a - lo;
+  t1 = ee - lo;
+}
+
+// Warp-wide spin: lane l waits until flag(l) >= target(l) (target 0: nothing to wait for), acquire
+// at system scope (peers publish over NVLink) or GPU scope; ~10 s timeout raises *err.
+__device__ __forceinline__ bool wait_flags_warp(const unsigned long long* flag, unsigned long long target, bool sys,
+                                                int* err) {
+  unsigned long long t0 = gtimer();
+  for (;;) {
+    unsigned long long v = ~0ull;
+    if (target) {
+      if (sys) asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+      else asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+    }
+    if (__all_sync(0xffffffffu, v >= target)) return true;
+    const bool late = gtimer() - t0 > 10000000000ull || *(volatile int*)err;
+    if (__any_sync(0xffffffffu, late)) {
+      if ((threadIdx.x & 31) == 0) atomicExch(err, 1);
+      return false;
+    }
+    __nanosleep(64);
+  }
+}
+
 template <int DT, int SR>
-__global__ void __launch_bounds__(kK3Threads) k5_persistent(PersistArgs pa) {
+__global__ void __launch_bounds__(kK3Threads, sizeof(typename Tr<DT, SR>::D) == 4 ? 3 : 2)   // 32-bit: 3 CTAs per SM, else 2
+    k5_persistent(PersistArgs pa) {
   using T = Tr<DT, SR>;
   using L = typename T::L;
   using G = typename T::G;
@@ -520,75 +602,114 @@ __global__ void __launch_bounds__(kK3Threads) k5_persistent(PersistArgs pa) {
   G* sG2 = reinterpret_cast<G*>(smem + lay.g2Off);
   __shared__ int64_t s_tile;
   __shared__ int s_flag;
+  __shared__ __align__(8) unsigned long long s_mbar;   // bulk-copy completion (one phase per valid tile)
+  uint32_t mphase = 0;
   const int64_t ntiles = pa.nentries * B;
+  if (tid == 0) {
+    mbar_init(&s_mbar);
+    s_tile = (int64_t)atomicAdd(pa.counter, 1ull);
+  }
   for (;;) {
-    if (tid == 0) s_tile = (int64_t)atomicAdd(pa.counter, 1ull);
     __syncthreads();
     const int64_t tile = s_tile;
     if (tile >= ntiles) break;
-    unsigned long long* tr = pa.trace ? pa.trace + 4 * tile : nullptr;
+    unsigned long long* tr = pa.trace ? pa.trace + 6 * tile : nullptr;
     if (tr && tid == 0) tr[0] = gtimer();
     const int4 tl = pa.tiles[tile / B];
     const int b = (int)(tile % B);
-    const int j = tl.x, blk = tl.y, q = tl.z, nch = tl.w;
+    // {j, blk | nch << 16, k0, k1}: splits [k0, k1) of column block blk (nch chunks, <= kc each)
+    const int j = tl.x, blk = tl.y & 0xffff, nch = tl.y >> 16, k0 = tl.z, k1 = tl.w;
     const int imax_layer = n - m + j;
-    const int cbase = j & ~3, kstart = (j - 1) & ~3;
+    const int cbase = j & ~3;
     const int c0 = cbase + kK3Cols * blk;
     const int imaxb = min(c0 + kK3Cols - 1, imax_layer);
-    const int kend = align4(imaxb);
-    const int k0 = kstart + q * kc;
-    const int k1 = min(k0 + kc, kend);
     // invalid problems compute nothing but still count and publish their blocks, so that the
     // number of arrivals every rank expects does not depend on device-side validation
     const bool valid = a.status[b] == HEDDLE_OK;
-    // ---- dependencies: row j-1 columns [max(k0, j-1), min(k1-1, n-m+j-1)] final (row 1: prologue)
-    if (valid && j >= 3) {
-      if (tid == 0) {
-        const int pc = (j - 1) & ~3;
-        const int lo = max(k0, j - 1), hi = min(k1 - 1, n - m + j - 1);
-        int ok = 1;
-        for (int bb = (lo - pc) / kK3Cols; ok && bb <= (hi - pc) / kK3Cols; ++bb)
-          ok = wait_flag(pa.ready + ((int64_t)(j - 1) * B + b) * ncb + bb, pa.epoch, pa.err);
-        s_flag = ok;
-      }
-      __syncthreads();
-      if (!s_flag) break;
-    }
-    if (tr && tid == 0) tr[1] = gtimer();
+    const int2 rc = a.rowcap[(int64_t)b * m + j - 1];   // {profile row, cap} of worker j (prologue)
     const L* gL = reinterpret_cast<const L*>(a.lengths) + (int64_t)b * a.ls;
     const D* gprev = reinterpret_cast<const D*>(a.dpws) + ((int64_t)b * (m + 1) + (j - 1)) * (n + 1);
     D* gcur = reinterpret_cast<D*>(a.dpws) + ((int64_t)b * (m + 1) + j) * (n + 1);
-    if (valid) {
-    int row = 0;
-    const int d = a.degrees[(int64_t)b * a.ds + j - 1];
-    for (int qq = 0; qq < a.D; ++qq) row = (a.prof_deg[qq] == d) ? qq : row;
-    const G* grow = reinterpret_cast<const G*>(a.gtab) + (int64_t)row * a.gstride;
-    const int cap = a.caps ? a.caps[(int64_t)b * a.cs + j - 1] : -1;
-    const int ghi = (cap >= 0 && cap < n) ? cap : n;
-    for (int t = tid; t < kc + kK3LPad; t += kK3Threads) {
-      const int k = k0 + t;
-      const bool in = k < k1;
-      sdp[t] = in ? ld_cg(gprev + k) : T::inf();   // produced by other CTAs / peers: read at L2
-      sL[t] = in ? gL[k] : (L)1;
-    }
+    // stage only this chunk's extent (chunks on the diagonal are much shorter than kc)
+    const int kl = k1 - k0;
     const int s0 = c0 - k1 - kK3GPadLo;
-    for (int t = tid; t <= lay.gLen; t += kK3Threads) {
-      const int s = s0 + t;
-      const G g = (s >= 1 && s <= ghi) ? grow[s] : T::gpad();
-      if (t < lay.gLen) sG[t] = g;
-      if (t > 0) sG2[t - 1] = g;
+    const int gl = align4(kK3Cols + kl + kK3GPadLo + 16);   // == lay.gLen for a full chunk
+    // ---- L and the G window do not depend on row j-1: bulk copies (TMA) of L[k0, k1), G(s0 + t)
+    // and G(s0 + 1 + t) are issued by thread 0 and land while the dependency wait runs; threads
+    // write only the +inf / pad elements around them
+    if (valid) {
+      const G* grow = reinterpret_cast<const G*>(a.gtab) + (int64_t)rc.x * a.gstride;
+      const G* gA = reinterpret_cast<const G*>(pa.gA) + (int64_t)rc.x * pa.gsp;
+      const G* gB = reinterpret_cast<const G*>(pa.gB) + (int64_t)rc.x * pa.gsp;
+      const int cap = rc.y;
+      const int ghi = (cap >= 0 && cap < n) ? cap : n;
+      int a0, a1, b0, b1;
+      bulk_span(gA, s0, gl, ghi, a0, a1);
+      bulk_span(gB, s0 + 1, gl, ghi, b0, b1);
+      const bool lbulk = kl > 0 && !(reinterpret_cast<uintptr_t>(gL + k0) & 15);
+      if (tid == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // after the last tile's generic accesses
+        mbar_arrive_tx(&s_mbar, (lbulk ? kl * (uint32_t)sizeof(L) : 0u) + (uint32_t)(a1 - a0 + b1 - b0) * (uint32_t)sizeof(G));
+        if (lbulk) bulk_g2s(sL, gL + k0, kl * (uint32_t)sizeof(L), &s_mbar);
+        if (a1 > a0) bulk_g2s(sG + a0, gA + s0 + a0, (uint32_t)(a1 - a0) * sizeof(G), &s_mbar);
+        if (b1 > b0) bulk_g2s(sG2 + b0, gB + s0 + 1 + b0, (uint32_t)(b1 - b0) * sizeof(G), &s_mbar);
+      }
+      for (int t = lbulk ? kl + tid : tid; t < kl + kK3LPad; t += kK3Threads) sL[t] = t < kl ? __ldg(gL + k0 + t) : (L)1;
+      for (int t = tid; t < gl; t += kK3Threads) {
+        if (t < a0 || t >= a1) {
+          const int s = s0 + t;
+          sG[t] = (s >= 1 && s <= ghi) ? __ldg(grow + s) : T::gpad();
+        }
+        if (t < b0 || t >= b1) {
+          const int s = s0 + 1 + t;
+          sG2[t] = (s >= 1 && s <= ghi) ? __ldg(grow + s) : T::gpad();
+        }
+      }
+    }
+    if (tr && tid == 0) tr[1] = gtimer();
+    // ---- dependencies: row j-1 columns [max(k0, j-1), min(k1-1, n-m+j-1)] final (row 1: prologue);
+    // warp 0 polls the covering blocks' counters side by side (one lane per block)
+    if (warp == 0) {
+      int ok = 1;
+      if (valid && j >= 3) {
+        const int pc = (j - 1) & ~3;
+        const int lo = max(k0, j - 1), hi = min(k1 - 1, n - m + j - 1);
+        const int bb1 = (hi - pc) / kK3Cols;
+        for (int g = (lo - pc) / kK3Cols; ok && g <= bb1; g += 32) {
+          const int bb = g + lane;
+          const bool need = bb <= bb1;
+          // single GPU: every chunk of a block adds 1, final at its chunk count; split: 1 per solve
+          const unsigned long long target =
+              !need ? 0ull : pa.peer_dp ? pa.epoch : (unsigned long long)pa.nch[(j - 1) * ncb + bb];
+          ok = wait_flags_warp(pa.ready + ((int64_t)(j - 1) * B + b) * ncb + (need ? bb : 0), target,
+                               pa.peer_dp != nullptr, pa.err);
+        }
+      }
+      if (lane == 0) s_flag = ok;
     }
     __syncthreads();
+    if (!s_flag) break;
     if (tr && tid == 0) tr[2] = gtimer();
+    if (valid) {
+    mbar_wait(&s_mbar, mphase);   // the bulk copies of this tile (each thread observes completion)
+    mphase ^= 1u;
+    // row j-1 was produced by other CTAs / peers: read at L2, all loads in flight before the stores
+    stage_batched<kK3Threads, sizeof(D) == 4 ? 9 : 4>(kl + kK3LPad, [&](int t) { return t < kl ? ld_cg(gprev + k0 + t) : T::inf(); },
+                                 [&](int t, D v) { sdp[t] = v; });
+    __syncthreads();
+    if (tr && tid == 0) tr[3] = gtimer();
     const int cw = c0 + kWarpCols * warp;
-    if (cw <= imaxb) {
+    // the warp's own split range: splits at or above its top column only meet the +inf padding
+    // of G (the triangle k >= i), so they are skipped -- whole warps on the diagonal chunks
+    const int k1w = min(k1, align4(min(cw + kWarpCols - 1, imaxb)));
+    if (cw <= imaxb && k1w > k0) {
       const int c = cw + kLaneCols * cl;
-      const int Q = 4 * ((k1 - k0 + 4 * kSplitLanes - 1) / (4 * kSplitLanes));
+      const int Q = 4 * ((k1w - k0 + 4 * kSplitLanes - 1) / (4 * kSplitLanes));
       D acc[kLaneCols];
       int arg[kLaneCols], klo[kLaneCols];
 #pragma unroll
       for (int r = 0; r < kLaneCols; ++r) { acc[r] = T::inf(); arg[r] = -1; klo[r] = j - 1; }
-      check_sweep(kg * Q, Q / 4, kLaneCols, 0, kc + kK3LPad, 0, lay.gLen, c - s0 - k0);
+      check_sweep(kg * Q, Q / 4, kLaneCols, 0, kl + kK3LPad, 0, gl, c - s0 - k0);
       sweep_slide<DT, SR, false, false, kLaneCols>(sL - k0, sdp - k0, sG + (c - s0), sG2 + (c - s0), k0 + kg * Q,
                                                    Q / 4, acc, arg, klo);
 #pragma unroll
@@ -607,10 +728,22 @@ __global__ void __launch_bounds__(kK3Threads) k5_persistent(PersistArgs pa) {
       }
     }
     }   // valid
-    // ---- completion of the column block -> publish
+    // ---- completion of the column block -> publish.  The next tile is dequeued here, so its
+    // round trip overlaps the fence instead of starting the next iteration.
+    unsigned long long next = 0;
+    if (tr && tid == 0) tr[4] = gtimer();
+    if (tid == 0) next = atomicAdd(pa.counter, 1ull);
     __threadfence();
     __syncthreads();
     const int64_t bidx = ((int64_t)j * B + b) * ncb + blk;
+    if (!pa.peer_dp) {   // single GPU: count the chunk; consumers wait for the block's chunk count
+      if (tid == 0) {
+        atomicAdd(pa.ready + bidx, 1ull);
+        if (tr) tr[5] = gtimer();
+        s_tile = (int64_t)next;
+      }
+      continue;
+    }
     if (tid == 0) {
       s_flag = atomicAdd(pa.blk_done + bidx, 1u) == (unsigned)(nch - 1);
       if (s_flag && pa.peer_dp) s_flag = wait_flag(pa.start_flag, pa.wait_start, pa.err) ? 1 : 2;
@@ -638,8 +771,10 @@ __global__ void __launch_bounds__(kK3Threads) k5_persistent(PersistArgs pa) {
       }
       if (tid == 0) atomicAdd_system(pa.ready + bidx, 1ull);   // local consumers
     }
-    if (tr && tid == 0) tr[3] = gtimer();
-    __syncthreads();
+    if (tid == 0) {
+      if (tr) tr[5] = gtimer();
+      s_tile = (int64_t)next;
+    }
   }
 }
 

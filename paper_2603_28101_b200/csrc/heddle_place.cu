@@ -108,9 +108,13 @@ struct heddle_place_ctx {
   unsigned long long** d_peer_ready = nullptr; // device array [world]
   std::vector<void*> peer_ready_h;
   int4* d_tiles = nullptr;
+  int* d_nch = nullptr;                      // [m+1][ncb] chunks per column block of the cached tile list
+  int2* d_rowcap = nullptr;                   // [max_batch][max_m] {profile row, cap} (K3/K5 prologue)
+  void* d_gpad = nullptr;                     // K5 TMA staging: two row-padded copies of the cost table
+  int gsp = 0;                                //   (row stride gsp; copy A offset 3, copy B offset 2 elements)
   size_t tiles_cap = 0;
   int64_t tiles_n = 0;
-  int tiles_key[6] = {-1, -1, -1, -1, -1, -1};
+  int tiles_key[7] = {-1, -1, -1, -1, -1, -1, -1};
   int64_t ready_epoch = 0;                    // solves that used d_ready (single-GPU and split)
   unsigned long long arrive_total = 0;        // cumulative K5 arrivals expected (split mode)
   unsigned long long** d_peer_arrive = nullptr; // device array [world]: &peer_flags[r][max_m + 1]
@@ -269,28 +273,35 @@ heddle_status solve_persistent(heddle_place_ctx* x, SolveArgs& a, cudaStream_t s
       return HEDDLE_E_NOMEM;
     }
   }
-  // tile list (layer-major, chunk-major inside a layer; this rank's blocks only), cached per shape
-  const int key[6] = {n, m, kc, rank, world, ncb};
+  // tile list (layer-major; inside a layer ascending first split, then block; this rank's blocks
+  // only), cached per shape.  A block's splits [kstart, kend) are cut into chunks of kc, except the
+  // diagonal part [c0 - 4, kend): it reads row j-1's block of the same index -- the last one that
+  // layer finishes -- so it forms the dependency chain through the layers and is cut into small
+  // chunks of kd splits that run side by side on different SMs.
+  int kd = kc;   // (measured: small diagonal chunks did not shorten the solve, profiles/r01_k5_variants.jsonl)
+  if (const char* e = std::getenv("HEDDLE_PLACE_K5_KD")) kd = std::max(16, std::min(kc, std::atoi(e) & ~3));
+  const int key[7] = {n, m, kc, rank, world, ncb, kd};
   if (std::memcmp(key, x->tiles_key, sizeof(key)) != 0) {
     std::vector<int4> tl;
     const int nown = owned_slots(ncb, world);
     for (int j = 2; j <= m; ++j) {
       const int cbase = j & ~3, kstart = (j - 1) & ~3, imax = n - m + j;
-      int qmax = 0;
-      std::vector<std::pair<int, int>> blks;   // (blk, nch)
+      std::vector<int4> lt;   // {k0, blk, k1, nch}
       for (int sl = 0; sl < nown; ++sl) {
         const int blk = owned_block(sl, rank, world);
         const int c0 = cbase + kK3Cols * blk;
         if (blk >= ncb || c0 > imax || (j == m && c0 + kK3Cols <= n)) continue;
         const int kend = align4(std::min(c0 + kK3Cols - 1, imax));
-        const int nch = (kend - kstart + kc - 1) / kc;
-        blks.push_back({blk, nch});
-        qmax = std::max(qmax, nch);
+        const int tlo = kd < kc ? std::min(kend, std::max(kstart, c0 - 4)) : kend;
+        std::vector<std::pair<int, int>> ch;
+        for (int k0 = kstart; k0 < tlo; k0 += kc) ch.push_back({k0, std::min(k0 + kc, tlo)});
+        for (int k0 = tlo; k0 < kend; k0 += kd) ch.push_back({k0, std::min(k0 + kd, kend)});
+        for (auto& c : ch) lt.push_back(make_int4(c.first, blk, c.second, (int)ch.size()));
       }
-      std::sort(blks.begin(), blks.end());
-      for (int q = 0; q < qmax; ++q)
-        for (auto& bn : blks)
-          if (q < bn.second) tl.push_back(make_int4(j, bn.first, q, bn.second));
+      std::sort(lt.begin(), lt.end(), [](const int4& p, const int4& q) {
+        return p.x != q.x ? p.x < q.x : p.y < q.y;
+      });
+      for (auto& t : lt) tl.push_back(make_int4(j, t.y | (t.w << 16), t.x, t.z));
     }
     if (tl.size() > x->tiles_cap) {
       cudaFree(x->d_tiles);
@@ -300,6 +311,13 @@ heddle_status solve_persistent(heddle_place_ctx* x, SolveArgs& a, cudaStream_t s
       x->tiles_cap = tl.size();
     }
     if (!tl.empty() && cudaMemcpy(x->d_tiles, tl.data(), sizeof(int4) * tl.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+      return HEDDLE_E_CUDA;
+    std::vector<int> nchv((size_t)(m + 1) * ncb, 0);   // chunks per (layer, block)
+    for (auto& t : tl) nchv[(size_t)t.x * ncb + (t.y & 0xffff)] = t.y >> 16;
+    cudaFree(x->d_nch);
+    x->d_nch = nullptr;
+    if (cudaMalloc(&x->d_nch, sizeof(int) * nchv.size()) != cudaSuccess) { cudaGetLastError(); return HEDDLE_E_NOMEM; }
+    if (cudaMemcpy(x->d_nch, nchv.data(), sizeof(int) * nchv.size(), cudaMemcpyHostToDevice) != cudaSuccess)
       return HEDDLE_E_CUDA;
     x->tiles_n = (int64_t)tl.size();
     std::memcpy(x->tiles_key, key, sizeof(key));
@@ -312,11 +330,33 @@ heddle_status solve_persistent(heddle_place_ctx* x, SolveArgs& a, cudaStream_t s
       cudaMemsetAsync(x->d_ready, 0, 8 * (size_t)B * ncb * (m + 1), s) != cudaSuccess ||
       cudaMemsetAsync(x->d_err, 0, sizeof(int), s) != cudaSuccess)
     return HEDDLE_E_CUDA;
+  // cost-table copies for the bulk (TMA) staging of G windows: rows padded to a multiple of 4
+  // elements, copy A shifted by 3 and copy B by 2, so the windows K5 stages (start == 1 mod 4,
+  // and the one-element-shifted copy) begin on 16-byte boundaries
+  if (!x->d_gpad) {
+    const size_t es = elem_size(dt);
+    x->gsp = align4(x->gstride) + 4;
+    const size_t half = (size_t)x->D * x->gsp + 4;
+    if (cudaMalloc(&x->d_gpad, 2 * es * half) != cudaSuccess) { cudaGetLastError(); return HEDDLE_E_NOMEM; }
+    for (int c = 0; c < 2; ++c) {
+      char* dst = static_cast<char*>(x->d_gpad) + es * (c * half + (c == 0 ? 3 : 2));
+      if (cudaMemcpy2DAsync(dst, es * x->gsp, x->d_gtab, es * x->gstride, es * x->gstride, x->D,
+                            cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+        return HEDDLE_E_CUDA;
+    }
+  }
   PersistArgs pa{};
+  {
+    const size_t es = elem_size(dt), half = (size_t)x->D * x->gsp + 4;
+    pa.gA = static_cast<char*>(x->d_gpad) + es * 3;
+    pa.gB = static_cast<char*>(x->d_gpad) + es * (half + 2);
+    pa.gsp = x->gsp;
+  }
   pa.a = a;
   pa.kc = kc;
   pa.ncb = ncb;
   pa.tiles = x->d_tiles;
+  pa.nch = x->d_nch;
   pa.nentries = x->tiles_n;
   pa.counter = x->d_ctr;
   pa.blk_done = x->d_blkdone;
@@ -375,16 +415,16 @@ heddle_status solve_persistent(heddle_place_ctx* x, SolveArgs& a, cudaStream_t s
   const char* ttrace = std::getenv("HEDDLE_PLACE_TILE_TRACE");
   unsigned long long* d_trace = nullptr;
   if (ttrace && ttrace[0]) {
-    if (cudaMalloc(&d_trace, 32 * (size_t)ntiles) != cudaSuccess) { cudaGetLastError(); d_trace = nullptr; }
-    else cudaMemsetAsync(d_trace, 0, 32 * (size_t)ntiles, s);
+    if (cudaMalloc(&d_trace, 48 * (size_t)ntiles) != cudaSuccess) { cudaGetLastError(); d_trace = nullptr; }
+    else cudaMemsetAsync(d_trace, 0, 48 * (size_t)ntiles, s);
     pa.trace = d_trace;
   }
   fn<<<grid, kK3Threads, smem, s>>>(pa);
   x->launches++;
   if (d_trace) {
-    std::vector<unsigned long long> h(4 * (size_t)ntiles);
+    std::vector<unsigned long long> h(6 * (size_t)ntiles);
     std::vector<int4> tl(x->tiles_n);
-    cudaMemcpyAsync(h.data(), d_trace, 32 * (size_t)ntiles, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(h.data(), d_trace, 48 * (size_t)ntiles, cudaMemcpyDeviceToHost, s);
     cudaMemcpyAsync(tl.data(), x->d_tiles, sizeof(int4) * tl.size(), cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
     cudaFree(d_trace);
@@ -429,6 +469,10 @@ heddle_status solve_layered(heddle_place_ctx* x, SolveArgs& a, bool kp, bool kv,
     if (cudaMalloc(&x->d_ctr, 8 * (size_t)(x->max_m + 1)) != cudaSuccess) { cudaGetLastError(); return HEDDLE_E_NOMEM; }
   }
   if (cudaMemsetAsync(x->d_ctr, 0, 8 * (size_t)(m + 1), s) != cudaSuccess) return HEDDLE_E_CUDA;
+  if (!x->d_rowcap) {
+    if (cudaMalloc(&x->d_rowcap, sizeof(int2) * (size_t)x->max_batch * x->max_m) != cudaSuccess) { cudaGetLastError(); return HEDDLE_E_NOMEM; }
+  }
+  a.rowcap = x->d_rowcap;
   const int64_t cells = (int64_t)B * (m + 1) * (n + 1);
   const int fill_grid = (int)std::min<int64_t>((cells + 255) / 256, (int64_t)x->num_sms * 16);
   HP_DISPATCH(fill_launch, a, cells, fill_grid, s);
@@ -655,6 +699,9 @@ void heddle_place_destroy(heddle_place_ctx* ctx) {
   cudaFree(ctx->d_peer_arrive);
   cudaFree(ctx->d_ready);
   cudaFree(ctx->d_tiles);
+  cudaFree(ctx->d_nch);
+  cudaFree(ctx->d_rowcap);
+  cudaFree(ctx->d_gpad);
   cudaFree(ctx->d_flags);
   cudaFree(ctx->d_blkdone);
   cudaFree(ctx->d_err);
