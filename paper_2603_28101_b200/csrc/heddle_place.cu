@@ -11,6 +11,7 @@
 #include <cstring>
 #include <cstdio>
 #include <new>
+#include <string>
 #include <vector>
 #include <algorithm>
 
@@ -428,7 +429,8 @@ heddle_status solve_persistent(heddle_place_ctx* x, SolveArgs& a, cudaStream_t s
     cudaMemcpyAsync(tl.data(), x->d_tiles, sizeof(int4) * tl.size(), cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
     cudaFree(d_trace);
-    if (FILE* f = std::fopen(ttrace, "ab")) {   // record: int64 {ntiles, B, kc, grid, rank, world}, int4 tiles, u64 times
+    const std::string tpath = world > 1 ? std::string(ttrace) + ".r" + std::to_string(rank) : std::string(ttrace);
+    if (FILE* f = std::fopen(tpath.c_str(), "ab")) {   // record: int64 {ntiles, B, kc, grid, rank, world}, int4 tiles, u64 times
       const int64_t hdr[6] = {ntiles, B, kc, grid, rank, world};
       std::fwrite(hdr, sizeof(hdr), 1, f);
       std::fwrite(tl.data(), sizeof(int4), tl.size(), f);
