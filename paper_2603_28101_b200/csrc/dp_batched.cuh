@@ -411,8 +411,11 @@ template <int DT, int SR, bool KP, bool KV, bool W = false>
 #ifndef HEDDLE_K2_MINBLOCKS
 #define HEDDLE_K2_MINBLOCKS 1
 #endif
+#ifndef HEDDLE_K2_MINMAX_BLOCKS
+#define HEDDLE_K2_MINMAX_BLOCKS 4
+#endif
 // 32-bit min-max variants fit 128 registers without spilling: 4 CTAs (16 warps) per SM
-__global__ void __launch_bounds__(kK2Threads, (SR == HEDDLE_MINMAX && DT != HEDDLE_F64) ? 4 : HEDDLE_K2_MINBLOCKS)
+__global__ void __launch_bounds__(kK2Threads, (SR == HEDDLE_MINMAX && DT != HEDDLE_F64) ? HEDDLE_K2_MINMAX_BLOCKS : HEDDLE_K2_MINBLOCKS)
     k2_dp_batched(SolveArgs a) {
   using T = Tr<DT, SR>;
   using L = typename T::L;
