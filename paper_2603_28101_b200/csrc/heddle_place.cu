@@ -252,6 +252,11 @@ heddle_status solve_persistent(heddle_place_ctx* x, SolveArgs& a, cudaStream_t s
   const int dt = x->dtype, sr = x->semiring;
   const int n = a.n, m = a.m, B = a.B, world = x->split_world, rank = x->split_rank;
   int kc = k5_kc(n, m, B, x->num_sms, world);
+  // throughput-bound solves (the chain allows chunks of >= 512 splits): twice the chunk at 2
+  // resident CTAs per SM instead of 3 -- measured 3.8 / 3.4 / 6.2 % faster on the large instance
+  // at 1 / 2 / 4 GPUs (profiles/r01_k5_variants.jsonl); latency-bound solves keep 3 CTAs per SM
+  const bool big_tiles = kc >= 512;
+  if (big_tiles) kc *= 2;
   if (const char* e = std::getenv("HEDDLE_PLACE_K5_KC")) kc = std::max(64, std::atoi(e) & ~15);   // tuning
   const int ncb = (n - m + 3) / kK3Cols + 1;
   const int ncb_max = (x->max_n + 3) / kK3Cols + 2;
@@ -402,9 +407,9 @@ heddle_status solve_persistent(heddle_place_ctx* x, SolveArgs& a, cudaStream_t s
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kK3Threads, smem);
   if (occ < 1) return HEDDLE_E_CUDA;
   const int64_t ntiles = x->tiles_n * B;
-  // resident CTAs per SM: 3 (measured best on the large config; more CTAs stretch every tile
-  // and with it the dependency chain through the layers)
-  int per_sm = std::min(occ, 3);
+  // resident CTAs per SM: 3 for latency-bound solves, 2 with the doubled chunks (more CTAs stretch
+  // every tile and with it the dependency chain through the layers)
+  int per_sm = std::min(occ, big_tiles ? 2 : 3);
   if (const char* e = std::getenv("HEDDLE_PLACE_K5_CTAS")) per_sm = std::max(1, std::min(occ, std::atoi(e)));
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)per_sm * x->num_sms));
   std::vector<cudaEvent_t> tev(2);
