@@ -35,8 +35,46 @@ B_TOTAL, N, M = 16384, 1024, 32
 WORKLOAD = ("batched sweep (BASELINE configs[3]): 16384 independent N=1024 K=32 placement problems, "
             "coding(Pareto)/search(log-normal) families alternating, predicted FP32 lengths, random sorted "
             "MP degrees over {1,2,4,8}, Eq. 3 min-max")
+LARGE_WORKLOAD = ("single large instance (BASELINE configs[4]): N=65536 coding-like predicted lengths into "
+                  "K=256 workers, FP32, Eq. 3 min-max")
 SM_COUNT = 148
 ISSUE_SLOTS_PER_CELL = 3   # ALU cycles per warp-transition: FMNMX (2) + half an FMNMX3 (1); profiles/r01_alu_peaks.jsonl
+
+
+def transitions(n, m):
+    """W(n, m): the (state, split) transitions of Eq. 3 on the computed region (SURVEY §8a,
+    DESIGN.md §4) -- 2(n-m+1) + (m-2)(n-m+1)(n-m+2)/2 for m >= 2, 1 for m = 1, 0 for n < m.
+    Computed here so the oracle legs never load the CUDA library; the CUDA arm checks it against
+    heddle_place_transitions."""
+    if n < m or m < 1:
+        return 0
+    if m == 1:
+        return 1
+    return 2 * (n - m + 1) + (m - 2) * (n - m + 1) * (n - m + 2) // 2
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def bench_config(workload, world):
+    """The `config` object of both arms (identical for the same workload and N)."""
+    if workload == "batched":
+        return {"workload": WORKLOAD, "problems": B_TOTAL, "n": N, "m": M, "semiring": "minmax",
+                "transitions_per_problem": transitions(N, M),
+                "parallelism": f"dp{world} (problems block-sharded across ranks, no collective on the data path; "
+                               "results all-gathered inside the timed region)",
+                "l2": "flushed between timed steps (256 MiB device write, untimed)"}
+    return {"workload": LARGE_WORKLOAD, "problems": 1, "n": 65536, "m": 256, "semiring": "minmax",
+            "transitions_per_problem": transitions(65536, 256),
+            "parallelism": f"split{world} (zigzag 512-column blocks, one dp-row exchange per layer)",
+            "l2": "flushed between timed steps (256 MiB device write, untimed)"}
 
 
 def peaks():
@@ -129,39 +167,52 @@ def shard(B, world, rank):
 
 # ------------------------------------------------------------------------------ oracle arm
 def run_reference(args):
+    """The oracle as it stands (oracle/, plain FP64-emulating-FP32 DP), on the host cores, over a
+    bounded sample of the same workload per step.  Never loads the CUDA library."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
     import oracle
     from inputs import workloads as wl
-    from paper_2603_28101_b200 import _lib
     oracle.build()
     threads = os.cpu_count() or 1
     sample = args.ref_sample
-    batch = wl.config_batched()
-    W = _lib.transitions(N, M)
+    if args.workload == "batched":
+        batch = wl.config_batched()
+        W = transitions(N, M)
+    else:
+        batch = wl.config_large(n=args.ref_large_n, m=args.ref_large_m)
+        W = transitions(batch.n, batch.m)
     times = []
     for step in range(args.warmup + args.steps):
-        lo = (step * sample) % batch.B
-        idx = np.arange(lo, lo + sample) % batch.B
-        rws = np.stack([batch.profile.row_of(batch.degrees[b]) for b in idx])
         t = time.perf_counter()
-        oracle.solve_batch(batch.lengths[idx], batch.profile.T, batch.profile.F, rws, mode="f32", threads=threads)
+        if args.workload == "batched":
+            lo = (step * sample) % batch.B
+            idx = np.arange(lo, lo + sample) % batch.B
+            rws = np.stack([batch.profile.row_of(batch.degrees[b]) for b in idx])
+            _, _, used = oracle.solve_batch(batch.lengths[idx], batch.profile.T, batch.profile.F, rws, mode="f32",
+                                            threads=threads)
+            units = sample * W
+        else:
+            oracle.solve(oracle.Problem.from_batch(batch, 0, mode="f32"), threads=threads)
+            used, units = threads, W
         dt = time.perf_counter() - t
         if step >= args.warmup:
             times.append(dt)
     tot = sum(times)
-    value = sample * W * len(times) / tot
+    value = units * len(times) / tot
+    what = (f"{sample} problems of the batched sweep per step" if args.workload == "batched" else
+            f"one n={batch.n}, m={batch.m} prefix-size instance of the configs[4] generator per step")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "problems": B_TOTAL, "n": N, "m": M, "semiring": "minmax",
-                   "parallelism": "host OpenMP over problems"},
-        "solves_per_s": sample * len(times) / tot,
-        "cpu_baseline": {"value": value, "unit": "cells/s", "cores": threads, "kind": "oracle",
-                         "sample": f"{sample} problems of the batched sweep per step (FP32-emulating FP64 oracle, "
-                                   f"plain O(n^2 m) DP with back-pointers)"},
+        "config": bench_config(args.workload, args.gpus),
+        "solves_per_s": (sample if args.workload == "batched" else 1) * len(times) / tot,
+        "cpu_baseline": {"value": value, "unit": "cells/s", "cores": used, "kind": "oracle", "cpu_model": cpu_model(),
+                         "sample": f"{what} (FP32-emulating FP64 oracle, plain O(n^2 m) DP with back-pointers, "
+                                   f"OpenMP over {'problems' if args.workload == 'batched' else 'columns'}); "
+                                   "value = cells of the sample / wall time"},
         "e2e": {"value": value, "unit": "cells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -171,7 +222,6 @@ def cpu_baseline(sample=64):
     """The oracle as it stands, on a bounded sample of the workload, on all host cores."""
     import oracle
     from inputs import workloads as wl
-    from paper_2603_28101_b200 import _lib
     oracle.build()
     threads = os.cpu_count() or 1
     batch = wl.config_batched(B=sample, seed_problem=1)
@@ -179,8 +229,54 @@ def cpu_baseline(sample=64):
     t = time.perf_counter()
     _, _, used = oracle.solve_batch(batch.lengths, batch.profile.T, batch.profile.F, rws, mode="f32", threads=threads)
     dt = time.perf_counter() - t
-    return {"value": sample * _lib.transitions(N, M) / dt, "unit": "cells/s", "cores": used, "kind": "oracle",
+    return {"value": sample * transitions(N, M) / dt, "unit": "cells/s", "cores": used, "kind": "oracle",
+            "cpu_model": cpu_model(),
             "sample": f"{sample} problems (n={N}, m={M}) of the batched-sweep workload, {dt:.1f} s wall"}
+
+
+def latency_lines(dev, reps=20):
+    """Device latency of the paper's own call shapes (solve + backtrack, CUDA events on the
+    launching stream, median of `reps` after warm-up): configs[1] rollout, configs[2] TP sweep and
+    the paper's §6.2 size (n = 6400, m = 16; the paper quotes ~42 ms on its CPU)."""
+    import torch
+    from inputs import workloads as wl
+    from paper_2603_28101_b200.placer import Placer
+    rng = np.random.default_rng(3)
+    L6400 = wl.presort(wl.predicted(rng, wl.coding_lengths(rng, 800, 8))).astype(np.float32)[None, :]
+    cfgs = [("rollout configs[1] (512, 32)", wl.config_rollout()),
+            ("tp_sweep configs[2] 4 x (4096, 64)", wl.config_tp_sweep()),
+            ("paper_6.2 (6400, 16)", wl.Batch("paper_6.2", 6400, 16, L6400, np.ones((1, 16), np.int32),
+                                              wl.float_profile()))]
+    out = {}
+    stream = torch.cuda.current_stream(dev)
+    for name, b in cfgs:
+        res = {}
+        for algo in ("scan", "valley"):
+            pl = Placer.from_profile(b.profile, max_n=b.n, max_m=b.m, max_batch=b.B, device=dev.index, algo=algo)
+            L = torch.from_numpy(b.lengths).to(dev)
+            D = torch.from_numpy(b.degrees.astype(np.int32)).to(dev)
+            for _ in range(3):
+                pl.solve(L, D)
+                pl.backtrack()
+            torch.cuda.synchronize()
+            ts, tb = [], []
+            for _ in range(reps):
+                e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+                e[0].record(stream)
+                pl.solve(L, D)
+                e[1].record(stream)
+                pl.backtrack()
+                e[2].record(stream)
+                torch.cuda.synchronize()
+                ts.append(e[0].elapsed_time(e[1]) * 1e3)
+                tb.append(e[1].elapsed_time(e[2]) * 1e3)
+            W = b.B * transitions(b.n, b.m)
+            t = statistics.median([a + c for a, c in zip(ts, tb)])
+            res[algo] = {"us": round(t, 1), "us_solve": round(statistics.median(ts), 1),
+                         "us_backtrack": round(statistics.median(tb), 1), "cells_per_s": W / (t * 1e-6)}
+            pl.close()
+        out[name] = res
+    return out
 
 
 # ------------------------------------------------------------------------------ CUDA arm
@@ -200,21 +296,18 @@ def run_cuda(args):
     if args.workload == "batched":
         lo, hi = shard(B_TOTAL, world, rank)
         batch = wl.config_batched()
-        n_, m_, b_total, workload = N, M, B_TOTAL, WORKLOAD
-        parallelism = f"dp{world} (problems block-sharded, no collective)"
+        n_, m_, b_total = N, M, B_TOTAL
         kernel_name = "k2_dp_batched<F32,MINMAX>"
     else:   # configs[4]: one n=65536, m=256 instance, columns split across ranks (one row exchange per layer)
         batch = wl.config_large()
         lo, hi = 0, 1
         n_, m_, b_total = batch.n, batch.m, 1
-        workload = ("single large instance (BASELINE configs[4]): N=65536 coding-like predicted lengths into "
-                    "K=256 workers, FP32, Eq. 3 min-max")
         if os.environ.get("HEDDLE_PLACE_EXCHANGE", "") == "nccl":
-            parallelism = f"split{world} (zigzag 512-column blocks, per-layer NCCL all-gather of the dp row)"
+            exchange = "per-layer NCCL all-gather of the dp row"
             kernel_name = "k3_layer<F32,MINMAX>"
         else:
-            parallelism = (f"split{world} (zigzag 512-column blocks; fused exchange: the tile finishing a block "
-                           "stores it into every peer's dp row over NVLink peer memory)")
+            exchange = ("fused: the tile finishing a block stores it into every peer's dp row over NVLink peer "
+                        "memory")
             kernel_name = "k5_persistent<F32,MINMAX>"
     Bl = hi - lo
     L = torch.from_numpy(np.ascontiguousarray(batch.lengths[lo:hi])).to(dev)
@@ -231,9 +324,16 @@ def run_cuda(args):
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
 
+    gather = world > 1 and args.workload == "batched"
+    if gather:
+        from paper_2603_28101_b200.dist import gather_shards
+
     def step():
-        placer.solve(L, D)
-        placer.backtrack()
+        obj, _ = placer.solve(L, D)
+        bnd = placer.backtrack()
+        if gather:   # the result gather of §8d: every rank ends with all B objectives and boundaries
+            gather_shards(obj, B_TOTAL)
+            gather_shards(bnd, B_TOTAL)
 
     for _ in range(args.warmup):
         step()
@@ -247,9 +347,12 @@ def run_cuda(args):
         for s in range(args.steps):
             flush.fill_(float(s))                      # L2 flush between timed iterations (not timed)
             ev[s][0].record(stream)
-            placer.solve(L, D)
+            obj, _ = placer.solve(L, D)
             ev[s][1].record(stream)
-            placer.backtrack()
+            bnd = placer.backtrack()
+            if gather:
+                gather_shards(obj, B_TOTAL)
+                gather_shards(bnd, B_TOTAL)
             ev[s][2].record(stream)
         torch.cuda.synchronize()
     launches = placer.launches - launches0
@@ -258,7 +361,8 @@ def run_cuda(args):
     torch.cuda.synchronize()
     t_step = sum(e[0].elapsed_time(e[2]) for e in ev) / 1e3          # seconds, K steps
     t_k2 = sum(e[0].elapsed_time(e[1]) for e in ev) / 1e3            # dominant kernel(s): the solve
-    W = _lib.transitions(n_, m_)
+    W = transitions(n_, m_)
+    assert W == _lib.transitions(n_, m_), "bench.transitions disagrees with heddle_place_transitions"
 
     # end to end through the public API with host buffers (H2D + solve + backtrack + D2H each step)
     for _ in range(2):
@@ -321,9 +425,7 @@ def run_cuda(args):
             "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * t_step / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": workload, "problems": b_total, "n": n_, "m": m_, "semiring": "minmax",
-                       "transitions_per_problem": W, "parallelism": parallelism,
-                       "l2": "flushed between timed steps (256 MiB device write, untimed)"},
+            "config": bench_config(args.workload, world),
             "solves_per_s": b_total * args.steps / t_step,
             "roofline": {"bound": "alu", "achieved": k2_rate / 1e9, "peak": peak / 1e9, "unit": "Gcell/s",
                          "frac": k2_rate / peak,
@@ -345,6 +447,10 @@ def run_cuda(args):
                 "ms_per_step": 1e3 * t_valley / args.steps, "solves_per_s": b_total * args.steps / t_valley,
                 "dp_equivalent_cells_per_s": cells / t_valley, "speedup_vs_scan": t_step / t_valley,
                 "identical_to_scan": same}
+        if args.workload == "large":
+            line["exchange"] = exchange
+        if not args.no_latency and args.workload == "batched":
+            line["latency"] = latency_lines(dev)
         if not args.no_cpu_baseline and world == 1 and args.workload == "batched":
             line["cpu_baseline"] = cpu_baseline(args.cpu_sample)
         print(json.dumps(line), flush=True)
@@ -362,6 +468,9 @@ def main():
     ap.add_argument("--workload", default="batched", choices=["batched", "large"],
                     help="batched = configs[3] (the metric's batched sweep, default); large = configs[4] split")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-latency", action="store_true", help="skip the paper-call-shape latency lines")
+    ap.add_argument("--ref-large-n", type=int, default=16384, help="reference arm, --workload large: sample size")
+    ap.add_argument("--ref-large-m", type=int, default=64)
     ap.add_argument("--no-valley", dest="valley", action="store_false",
                     help="skip the valley-solver line (HEDDLE_VALLEY) reported beside the scan")
     ap.add_argument("--cpu-sample", type=int, default=2048)

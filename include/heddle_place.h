@@ -157,6 +157,20 @@ heddle_status heddle_place_solve(heddle_place_ctx* ctx, const heddle_place_probl
 heddle_status heddle_place_backtrack(heddle_place_ctx* ctx, int32_t* boundaries_out,
                                      int32_t* parents_out, void* stream);
 
+/* Sampled states of the last solve (parity checks at sizes where the full back-pointer table
+ * is not exported; sub-problem optima).  For each query q (device int32 arrays of nq entries):
+ * problem qb[q], layer qj[q] in 1..m, column qi[q] (items [0, qi) in qj groups) ->
+ *   dp_out[q]      = dp[qj][qi] of that problem, the dtype of objective_out (Eq. 3);
+ *   parents_out[q] = parent[qj][qi], the LOWEST k in [qj-1, qi-1] attaining it (R3),
+ *                    recomputed from dp row qj-1 with the solve's own arithmetic, so it equals
+ *                    a stored back-pointer table bit for bit.
+ * States outside the computed region (qi outside [qj, n-m+qj], R8), of failed problems, or
+ * infeasible give parent -1 and dp = +inf / UINT max.  Works after every solve path (batched,
+ * layered, valley, split).  The problem buffers of the solve must still be alive.  Asynchronous
+ * on `stream`.  E_STATE before any solve; E_INVALID for null arrays with nq > 0 or nq < 0. */
+heddle_status heddle_place_query(heddle_place_ctx* ctx, int32_t nq, const int32_t* qb, const int32_t* qj,
+                                 const int32_t* qi, void* dp_out, int32_t* parents_out, void* stream);
+
 /* End-to-end convenience with HOST buffers: copies the problem arrays (host
  * pointers, same layout as heddle_place_problem) to the device, solves,
  * backtracks, copies objective / boundaries / status back to host memory and

@@ -161,9 +161,11 @@ def config_tp_sweep(problem: int = 0, n=4096, m=64) -> Batch:
     return Batch("tp_sweep", n, m, np.ascontiguousarray(lengths), deg, float_profile())
 
 
-def config_batched(B: int = 16384, n: int = 1024, m: int = 32, seed_problem: int = 0) -> Batch:
+def config_batched(B: int = 16384, n: int = 1024, m: int = 32, seed_problem: int = 0, dtype: str = "f32") -> Batch:
     """configs[3]: B independent N=1024 K=32 problems; coding / search families
-    alternate; random sorted degree vectors over {1,2,4,8} (SA candidates)."""
+    alternate; random sorted degree vectors over {1,2,4,8} (SA candidates).
+    dtype "f32" (the bench): noisy predicted lengths; "f64": the same predictions unrounded;
+    "u32": the true integer token lengths with the integer profile (bit-exact mode)."""
     rng = rng_for(3, seed_problem)
     prompts = n // 8
     base_c = 600.0 * (1.0 + rng.pareto(1.2, size=(B, prompts)))
@@ -173,17 +175,26 @@ def config_batched(B: int = 16384, n: int = 1024, m: int = 32, seed_problem: int
     search = np.clip(np.rint(np.exp(mu_s[:, :, None] + 0.6 * z)), 32, MAX_TOKENS)
     fam = (np.arange(B) % 2 == 0)[:, None, None]
     L = np.where(fam, coding, search).reshape(B, n)
-    Lhat = (L * np.exp(0.5 * rng.standard_normal((B, n)))).astype(np.float32)
-    lengths = presort_rows(Lhat)
+    Lhat = L * np.exp(0.5 * rng.standard_normal((B, n)))
     deg = sorted_degree_vectors(rng, B, m)
-    return Batch("batched", n, m, lengths, deg, float_profile())
+    if dtype == "u32":
+        return Batch("batched", n, m, presort_rows(L).astype(np.uint32), deg, int_profile())
+    if dtype == "f64":
+        return Batch("batched", n, m, presort_rows(Lhat), deg, float_profile(dtype="f64"))
+    return Batch("batched", n, m, presort_rows(Lhat.astype(np.float32)), deg, float_profile())
 
 
-def config_large(problem: int = 0, n: int = 65536, m: int = 256) -> Batch:
-    """configs[4]: single N=65536 K=256 instance (coding-like), degree 1."""
+def config_large(problem: int = 0, n: int = 65536, m: int = 256, dtype: str = "f32") -> Batch:
+    """configs[4]: single N=65536 K=256 instance (coding-like), degree 1.  dtype "u32": the true
+    integer token lengths with the integer profile; "f64": the same predictions as doubles."""
     rng = rng_for(4, problem)
-    L = presort(predicted(rng, coding_lengths(rng, n // 8, 8)))
+    true = coding_lengths(rng, n // 8, 8)
+    L = presort(predicted(rng, true))
     deg = np.ones((1, m), dtype=np.int32)
+    if dtype == "u32":
+        return Batch("large", n, m, presort(true)[None, :].astype(np.uint32), deg, int_profile())
+    if dtype == "f64":
+        return Batch("large", n, m, L[None, :].astype(np.float64), deg, float_profile(dtype="f64"))
     return Batch("large", n, m, L[None, :].astype(np.float32), deg, float_profile())
 
 

@@ -60,6 +60,7 @@ def lib():
         P = ctypes.POINTER(_Problem)
         vp = ctypes.c_void_p
         _lib.ora_solve.argtypes = [P, vp, vp, vp, vp]
+        _lib.ora_solve_threads.argtypes = [P, vp, vp, vp, vp, ctypes.c_int32]
         _lib.ora_group_cost.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_int]
         _lib.ora_group_cost.restype = ctypes.c_double
         _lib.ora_brute_contiguous.argtypes = [P, vp, vp, vp]
@@ -110,13 +111,18 @@ class Problem:
                    semiring=semiring, caps=caps, kvcaps=kv, w=w)
 
 
-def solve(p: Problem, want_tables=False):
+def solve(p: Problem, want_tables=False, threads=1):
+    """The DP (ora_solve).  threads > 1 shares each layer's columns over OpenMP threads
+    (ora_solve_threads); the result is identical."""
     n, m = p.n, p.m
     dp = np.empty((m + 1, n + 1), dtype=np.float64) if want_tables else None
     par = np.empty((m + 1, n + 1), dtype=np.int32) if want_tables else None
     b = np.empty(m + 1, dtype=np.int32)
     opt = np.zeros(1, dtype=np.float64)
-    st = lib().ora_solve(ctypes.byref(p.s), _ptr(dp), _ptr(par), _ptr(b), _ptr(opt))
+    if threads == 1:
+        st = lib().ora_solve(ctypes.byref(p.s), _ptr(dp), _ptr(par), _ptr(b), _ptr(opt))
+    else:
+        st = lib().ora_solve_threads(ctypes.byref(p.s), _ptr(dp), _ptr(par), _ptr(b), _ptr(opt), threads)
     return dict(status=st, opt=float(opt[0]), bounds=b, dp=dp, parent=par)
 
 

@@ -160,8 +160,20 @@ static int valid_problem(const ora_problem* p) {
  * (row j = layer j), either may be NULL.  bounds is [m+1]:  b_0 = 0 < ... <
  * b_m = n, b_{j-1} = parent[j][b_j].  Returns ORA_INFEASIBLE when OPT = +inf.
  */
+int ora_solve_threads(const ora_problem* p, double* dp_out, int32_t* parent_out,
+                      int32_t* bounds, double* opt, int32_t nthreads);
+
 int ora_solve(const ora_problem* p, double* dp_out, int32_t* parent_out,
               int32_t* bounds, double* opt) {
+  return ora_solve_threads(p, dp_out, parent_out, bounds, opt, 1);
+}
+
+/* The same DP with the columns i of one layer shared out over `nthreads` OpenMP threads (the
+ * states of a layer are independent: each reads only row j-1).  The arithmetic and the order of
+ * the k loop of every state are unchanged, so the result is identical to ora_solve's.  Used to
+ * write the configs[4] golden file (tests/golden/make_large_golden.py). */
+int ora_solve_threads(const ora_problem* p, double* dp_out, int32_t* parent_out,
+                      int32_t* bounds, double* opt, int32_t nthreads) {
   if (!valid_problem(p)) return ORA_INVALID;
   const int n = p->n, m = p->m;
   if (n < m) { *opt = ORA_INF; return ORA_INFEASIBLE; }
@@ -173,6 +185,9 @@ int ora_solve(const ora_problem* p, double* dp_out, int32_t* parent_out,
   for (size_t c = 0; c < cells; ++c) { dp[c] = ORA_INF; par[c] = -1; }
   dp[0] = 0.0;                                               /* dp[0][0] = 0 */
   for (int j = 1; j <= m; ++j) {
+#ifdef _OPENMP
+#pragma omp parallel for schedule(dynamic, 16) num_threads(nthreads > 0 ? nthreads : 1) if (nthreads > 1)
+#endif
     for (int i = j; i <= n - (m - j); ++i) {                 /* R8 */
       double best = ORA_INF;
       int arg = -1;

@@ -26,7 +26,8 @@ DTYPES = {"u32": U32, "f32": F32, "f64": F64}
 SEMIRINGS = {"minmax": MINMAX, "minplus": MINPLUS}
 
 # exported symbols declared in include/heddle_place.h (tests check the .so exports all of them)
-SYMBOLS = ("heddle_place_init", "heddle_place_solve", "heddle_place_backtrack", "heddle_place_solve_host",
+SYMBOLS = ("heddle_place_init", "heddle_place_solve", "heddle_place_backtrack", "heddle_place_query",
+           "heddle_place_solve_host",
            "heddle_place_launch_count", "heddle_place_transitions", "heddle_place_destroy",
            "heddle_place_strerror", "heddle_place_nccl_unique_id", "heddle_place_init_split",
            "heddle_place_split_blocks", "heddle_place_debug_violations", "heddle_place_retarget",
@@ -74,6 +75,8 @@ def lib() -> ctypes.CDLL:
         L.heddle_place_solve.restype = ctypes.c_int
         L.heddle_place_backtrack.argtypes = [vp, vp, vp, vp]
         L.heddle_place_backtrack.restype = ctypes.c_int
+        L.heddle_place_query.argtypes = [vp, ctypes.c_int32, vp, vp, vp, vp, vp, vp]
+        L.heddle_place_query.restype = ctypes.c_int
         L.heddle_place_solve_host.argtypes = [vp, ctypes.POINTER(Problem), vp, vp, vp, vp,
                                               ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
         L.heddle_place_solve_host.restype = ctypes.c_int

@@ -32,7 +32,10 @@ __device__ int first_within_target(const typename Tr<DT, SR>::L* __restrict__ gL
     const int k = a0 + lane * step;
     const bool ok = k < b0 && T::norm(T::comb(T::zero(), gL[k], grow[gsize(gWp, cur, k)])) <= target;
     const unsigned msk = __ballot_sync(0xffffffffu, ok);
-    if (msk == 0) { a0 = min(b0, a0 + 31 * step + 1); continue; }
+    if (msk == 0) {   // every probe made failed: continue past the last one actually made
+      a0 += min(31, (b0 - 1 - a0) / step) * step + 1;
+      continue;
+    }
     const int t = __ffs(msk) - 1;
     if (t == 0) { b0 = a0; break; }
     const int na = a0 + (t - 1) * step + 1;
@@ -183,7 +186,9 @@ __global__ void __launch_bounds__(kK4CtaThreads) k4_backtrack_cta(SolveArgs a, i
       mine = __reduce_min_sync(0xffffffffu, mine);
       if (lane == 0 && mine != INT_MAX) atomicMin(&s_found, mine);
       __syncthreads();
-      if (s_found != INT_MAX) break;
+      const int f = s_found;   // every thread reads before any can write it in the next round
+      __syncthreads();
+      if (f != INT_MAX) break;
     }
     const int found = s_found;
     __syncthreads();
@@ -195,6 +200,67 @@ __global__ void __launch_bounds__(kK4CtaThreads) k4_backtrack_cta(SolveArgs a, i
     if (tid == 0) out[j - 1] = cur;
   }
   if (tid == 0) out[0] = 0;
+}
+
+
+// State query (heddle_place_query): for sampled states (b, j, i) of the last solve, the stored
+// dp[j][i] and its back-pointer parent[j][i] = the lowest k in [j-1, i-1] attaining it (R3),
+// recomputed from row j-1 exactly as K4 does for the states on the optimal path.  One warp per
+// query.  Out-of-region states (i outside [j, n-m+j], R8), failed problems and infeasible states
+// give parent -1 and dp = the dtype's infinity (U32 MINPLUS: UINT64_MAX, as the objective).
+template <int DT, int SR, bool KV, bool W = false>
+__global__ void __launch_bounds__(32 * kK4Warps) k4_query(SolveArgs a, int nq, const int32_t* __restrict__ qb,
+                                                         const int32_t* __restrict__ qj,
+                                                         const int32_t* __restrict__ qi, void* dp_out,
+                                                         int32_t* __restrict__ par_out) {
+  using T = Tr<DT, SR>;
+  using L = typename T::L;
+  using G = typename T::G;
+  using D = typename T::D;
+  using S = typename SpT<DT>::type;
+  const int lane = threadIdx.x & 31;
+  const int q = blockIdx.x * kK4Warps + (threadIdx.x >> 5);
+  if (q >= nq) return;
+  const int n = a.n, m = a.m;
+  const int b = qb[q], j = qj[q], cur = qi[q];
+  D val = T::inf();
+  int found = -1;
+  const bool ok = b >= 0 && b < a.B && j >= 1 && j <= m && cur >= j && cur <= n - m + j &&
+                  (j < m || cur == n || m == 1) && a.status[b] == HEDDLE_OK;
+  if (ok) {
+    const D* gdp = reinterpret_cast<const D*>(a.dpws) + (int64_t)b * (m + 1) * (n + 1);
+    val = T::norm(gdp[(int64_t)j * (n + 1) + cur]);
+    if (val != T::inf()) {
+      if (j == 1) {
+        found = 0;   // layer 1: the only split is k = 0
+      } else {
+        const L* gL = reinterpret_cast<const L*>(a.lengths) + (int64_t)b * a.ls;
+        const G* gtab = reinterpret_cast<const G*>(a.gtab);
+        const S* gSp = KV ? reinterpret_cast<const S*>(a.spws) + (int64_t)b * (n + 1) : nullptr;
+        const int32_t* gWp = W ? a.wpws + (int64_t)b * (n + 1) : nullptr;
+        const int d = a.degrees[(int64_t)b * a.ds + j - 1];
+        int row = 0;
+        for (int r = 0; r < a.D; ++r) row = (a.prof_deg[r] == d) ? r : row;
+        const G* grow = gtab + (int64_t)row * a.gstride;
+        int lo = split_lower_bound<DT, KV>(a, b, j, cur, gSp, gWp);
+        lo = first_within_target<DT, SR>(gL, grow, lo, cur, val, lane, gWp);
+        for (int base = lo; base < cur && found < 0; base += 32) {
+          const int k = base + lane;
+          bool hit = false;
+          if (k < cur) hit = (T::norm(T::comb(gdp[(int64_t)(j - 1) * (n + 1) + k], gL[k], grow[gsize(gWp, cur, k)])) == val);
+          const unsigned msk = __ballot_sync(0xffffffffu, hit);
+          if (msk) found = base + __ffs(msk) - 1;
+        }
+      }
+    }
+  }
+  if (lane == 0) {
+    par_out[q] = found;
+    if constexpr (DT == HEDDLE_U32 && SR == HEDDLE_MINPLUS)
+      reinterpret_cast<uint64_t*>(dp_out)[q] = (val == T::inf()) ? ~0ull : val;
+    else
+      reinterpret_cast<D*>(dp_out)[q] = val;
+  }
 }
 
 }  // namespace hp

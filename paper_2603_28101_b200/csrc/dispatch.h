@@ -13,6 +13,7 @@
 
 using K2Fn = void (*)(hp::SolveArgs);
 using K4Fn = void (*)(hp::SolveArgs, int32_t*);
+using K4QFn = void (*)(hp::SolveArgs, int, const int32_t*, const int32_t*, const int32_t*, void*, int32_t*);
 using K3Fn = void (*)(hp::LayerArgs);
 using K5Fn = void (*)(hp::PersistArgs);
 using KPro = void (*)(hp::SolveArgs);
@@ -32,6 +33,7 @@ using K8SFn = void (*)(hp::SolveArgs, int, hp::ValleyWs);
 K2Fn k2_for(int dt, int sr, bool kp, bool kv, bool w = false);   // inst_k2.cu
 K4Fn k4_for(int dt, int sr, bool kv, bool w);                     // inst_k4.cu
 K4Fn k4c_for(int dt, int sr, bool kv, bool w);
+K4QFn k4q_for(int dt, int sr, bool kv, bool w);
 K3Fn k3_for(int dt, int sr, bool kp, bool kv);                    // inst_k35.cu
 KPro pro_for(int dt, int sr, bool kp, bool kv);
 K5Fn k5_for(int dt, int sr);

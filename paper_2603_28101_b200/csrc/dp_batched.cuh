@@ -70,7 +70,8 @@ struct SolveArgs {
   int32_t* status;         // [B] workspace status
   int32_t* status_out;     // [B] caller's status or null
   void* objective;         // [B] caller's objective
-  int* err;                // split mode: set by a peer-exchange timeout (reported as E_NCCL), or null
+  int* err;                // set by a dependency-wait timeout (layered kernels), or null
+  int split;               // world > 1: a timeout is a peer-exchange failure (E_NCCL), else E_CUDA
   // host-input pipeline (heddle_place_solve_host): problem b's inputs are resident once
   // ready[b / ready_chunk] == ready_epoch (written by the copy engine after the chunk's copies); null: resident
   const unsigned* ready;

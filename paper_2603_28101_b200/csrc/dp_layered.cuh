@@ -688,7 +688,10 @@ __global__ void __launch_bounds__(kK3Threads, sizeof(typename Tr<DT, SR>::D) == 
       if (lane == 0) s_flag = ok;
     }
     __syncthreads();
-    if (!s_flag) break;
+    if (!s_flag) {   // timed out: let this tile's bulk copies land before the CTA exits
+      if (valid) mbar_wait(&s_mbar, mphase);
+      break;
+    }
     if (tr && tid == 0) tr[2] = gtimer();
     if (valid) {
     mbar_wait(&s_mbar, mphase);   // the bulk copies of this tile (each thread observes completion)
@@ -766,6 +769,7 @@ __global__ void __launch_bounds__(kK3Threads, sizeof(typename Tr<DT, SR>::D) == 
           for (int r = 0; r < pa.own_world; ++r)
             if (r != pa.own_rank) {
               atomicAdd_system(pa.peer_ready[r] + bidx, 1ull);
+              __threadfence_system();   // the ready increment is visible before the arrival count
               atomicAdd_system(pa.peer_arrive[r], 1ull);   // total, for the end-of-solve barrier
             }
       }
@@ -828,7 +832,8 @@ __global__ void k3_finalize(SolveArgs a) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= a.B) return;
   const int n = a.n, m = a.m;
-  if (a.err && *(volatile int*)a.err) a.status[b] = HEDDLE_E_NCCL;   // peer exchange timed out
+  if (a.err && *(volatile int*)a.err)   // a dependency wait timed out: the rows are incomplete
+    a.status[b] = a.split ? HEDDLE_E_NCCL : HEDDLE_E_CUDA;
   if (a.status[b] != HEDDLE_OK) {
     if (a.status_out) a.status_out[b] = a.status[b];
     if constexpr (DT == HEDDLE_U32 && SR == HEDDLE_MINPLUS) reinterpret_cast<uint64_t*>(a.objective)[b] = ~0ull;

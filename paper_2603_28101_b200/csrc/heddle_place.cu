@@ -371,6 +371,9 @@ heddle_status solve_persistent(heddle_place_ctx* x, SolveArgs& a, cudaStream_t s
   pa.own_rank = rank;
   pa.own_world = world;
   pa.err = x->d_err;
+  pa.a.err = x->d_err;   // a dependency-wait timeout becomes an error status, not a silent partial row
+  a.err = x->d_err;
+  pa.a.split = a.split = world > 1;
   if (world > 1) {
     x->epoch++;
     if ((int)x->expect.size() < x->max_m + 1) x->expect.assign(x->max_m + 1, 0ull);
@@ -397,8 +400,6 @@ heddle_status solve_persistent(heddle_place_ctx* x, SolveArgs& a, cudaStream_t s
     pa.peer_arrive = x->d_peer_arrive;
     pa.arrive = x->d_flags + x->max_m + 1;
     pa.arrive_target = x->arrive_total;
-    pa.a.err = x->d_err;
-    a.err = x->d_err;
   }
   K5Fn fn = k5_for(dt, sr);
   const int smem = k3_smem(dt, sr, kc);
@@ -558,6 +559,7 @@ heddle_status solve_layered(heddle_place_ctx* x, SolveArgs& a, bool kp, bool kv,
     la.flags = x->d_flags;
     la.err = x->d_err;
     la.a.err = x->d_err;
+    la.a.split = 1;
     la.wait_start = x->expect[0];
   }
   for (int j = 2; j <= m; ++j) {
@@ -634,7 +636,7 @@ heddle_status solve_layered(heddle_place_ctx* x, SolveArgs& a, bool kp, bool kv,
                  "exchange %.3f ms (max %.1f us/layer)\n", x->split_rank, world, n, m, B, kc, grid, tk, tx, 1e3 * mx);
     for (auto& e : tev) cudaEventDestroy(e);
   }
-  if (p2p) a.err = x->d_err;
+  if (p2p) { a.err = x->d_err; a.split = 1; }
   HP_DISPATCH(finalize_launch, a, s);
   x->launches++;
   return cudaGetLastError() == cudaSuccess ? HEDDLE_OK : HEDDLE_E_CUDA;
@@ -1004,6 +1006,22 @@ heddle_status heddle_place_backtrack(heddle_place_ctx* x, int32_t* boundaries_ou
       return HEDDLE_E_CUDA;
   }
   return HEDDLE_OK;
+}
+
+heddle_status heddle_place_query(heddle_place_ctx* x, int32_t nq, const int32_t* qb, const int32_t* qj,
+                                 const int32_t* qi, void* dp_out, int32_t* parents_out, void* stream) {
+  if (!x || nq < 0 || (nq > 0 && (!qb || !qj || !qi || !dp_out || !parents_out))) return HEDDLE_E_INVALID;
+  if (!x->solved) return HEDDLE_E_STATE;
+  if (nq == 0) return HEDDLE_OK;
+  DeviceGuard guard(x->device);
+  const SolveArgs& a = x->last;
+  const int dt = x->dtype, sr = x->semiring;
+  (void)dt; (void)sr;
+  k4q_for(x->dtype, x->semiring, x->last_kv, x->last_w)<<<(nq + kK4Warps - 1) / kK4Warps, 32 * kK4Warps, 0,
+                                                          static_cast<cudaStream_t>(stream)>>>(a, nq, qb, qj, qi,
+                                                                                               dp_out, parents_out);
+  x->launches++;
+  return cudaGetLastError() == cudaSuccess ? HEDDLE_OK : HEDDLE_E_CUDA;
 }
 
 heddle_status heddle_place_solve_host(heddle_place_ctx* x, const heddle_place_problem* hp_, void* objective_host,

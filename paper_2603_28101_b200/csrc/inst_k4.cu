@@ -25,3 +25,11 @@ K4Fn k4_for(int dt, int sr, bool kv, bool w) {
 }
 
 K4Fn k4c_for(int dt, int sr, bool kv, bool w) { return HP_DISPATCH(pick_k4c, kv, w); }
+
+template <int DT, int SR>
+K4QFn pick_k4q(bool kv, bool w) {
+  if (w) return kv ? k4_query<DT, SR, true, true> : k4_query<DT, SR, false, true>;
+  return kv ? k4_query<DT, SR, true> : k4_query<DT, SR, false>;
+}
+
+K4QFn k4q_for(int dt, int sr, bool kv, bool w) { return HP_DISPATCH(pick_k4q, kv, w); }

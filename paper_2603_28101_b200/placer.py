@@ -165,6 +165,22 @@ class Placer:
                 "heddle_place_backtrack")
         return (bnd, par) if parents else bnd
 
+    def query(self, qb, qj, qi, stream=None):
+        """dp[j][i] and the lowest-index back-pointer parent[j][i] of sampled states (b, j, i) of the
+        last solve (heddle_place_query).  qb, qj, qi: int32 device tensors of equal length.
+        Returns (dp[nq] in the objective dtype, parent[nq] int32)."""
+        if self._last is None:
+            C.check(C.E_STATE, "heddle_place_query")
+        qb, qj, qi = (t.to(device=self.device, dtype=torch.int32).contiguous() for t in (qb, qj, qi))
+        nq = qb.numel()
+        dp = torch.empty(nq, dtype=self.objective_dtype, device=self.device)
+        par = torch.empty(nq, dtype=torch.int32, device=self.device)
+        s = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        C.check(C.lib().heddle_place_query(self._h, nq, _ptr(qb), _ptr(qj), _ptr(qi), _ptr(dp), _ptr(par),
+                                           ctypes.c_void_p(s)), "heddle_place_query")
+        self._keep_q = (qb, qj, qi)
+        return dp, par
+
     def solve_host(self, lengths, degrees, caps=None, kv_caps=None, stream=None, weights=None):
         """End to end with host (numpy / pinned torch CPU) buffers: H2D, solve, backtrack, D2H.
         Returns (objective, boundaries, status, bytes_h2d, bytes_d2h) as host arrays."""

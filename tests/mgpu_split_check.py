@@ -1,5 +1,7 @@
 """torchrun helper (not collected by pytest): split-mode solve of configs[4] over all ranks,
-compared bit for bit with a single-GPU solve on rank 0.  Prints SPLIT OK on success."""
+compared bit for bit with a single-GPU solve on rank 0 and, at the configs[4] size, on every rank
+with the oracle's stored solution (tests/golden/large_f32.npz: objective, boundaries and the
+sampled states' dp values and lowest-index back-pointers).  Prints SPLIT OK on success."""
 import os
 import sys
 
@@ -35,6 +37,20 @@ def main():
     allres = [torch.empty_like(res) for _ in range(world)]
     dist.all_gather(allres, res)
     ok = all(torch.equal(a, res) for a in allres)
+    gold = os.path.join(ROOT, "tests", "golden", "large_f32.npz")
+    if n == 65536 and m == 256 and os.path.exists(gold):
+        z = np.load(gold)
+        qd = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).cuda()
+        dp, par = pl.query(qd(np.zeros(z["qj"].size)), qd(z["qj"]), qd(z["qi"]))
+        torch.cuda.synchronize()
+        g_ok = (float(obj[0]) == float(z["opt"]) and np.array_equal(bnd.cpu().numpy()[0], z["bounds"])
+                and np.array_equal(dp.cpu().numpy().astype(np.float64), z["dp"])
+                and np.array_equal(par.cpu().numpy(), z["parent"]))
+        print(f"rank {rank}: oracle golden (objective, boundaries, {z['qj'].size} sampled dp values and "
+              f"back-pointers) identical={g_ok}", flush=True)
+        flag = torch.tensor([0 if g_ok else 1], device="cuda")
+        dist.all_reduce(flag)
+        ok = ok and int(flag.item()) == 0
     if rank == 0:
         ref = Placer.from_profile(batch.profile, max_n=n, max_m=m, max_batch=1, kernel="layered")
         o1, s1 = ref.solve(L, D)

@@ -100,19 +100,61 @@ def assert_f64_tolerance(gpu_obj, gpu_bounds, p64, semiring, tag=""):
     assert abs(gpu_obj - opt) <= REL_TOL * opt, (tag, gpu_obj, opt)
     cost = partition_cost_f64(p64, gpu_bounds, semiring)
     assert cost <= opt * (1 + REL_TOL), (tag, cost, opt)
-    # near-tie walk: at the first differing boundary the oracle's candidate values must tie
+    # near-tie walk: follow the GPU's own backtrack from layer m down to layer 1; at
+    # every layer where its split differs from the oracle's back-pointer of the SAME state, the
+    # oracle's candidate values of the two splits must tie within 1e-6 relative
     dp = ref["dp"]
-    rb = ref["bounds"]
-    m = len(rb) - 1
+    m = len(ref["bounds"]) - 1
+    assert gpu_bounds[m] == p64.n and gpu_bounds[0] == 0, (tag, gpu_bounds)
     for j in range(m, 1, -1):
-        if gpu_bounds[j - 1] == rb[j - 1] and gpu_bounds[j] == rb[j]:
-            continue
         i = int(gpu_bounds[j])
         kg = int(gpu_bounds[j - 1])
         ko = int(ref["parent"][j, i])
+        if kg == ko:
+            continue
 
         def v(k):
             c = oracle.group_cost(p64, j, k, i)
             return max(dp[j - 1, k], c) if semiring == "minmax" else dp[j - 1, k] + c
-        assert abs(v(kg) - v(ko)) <= REL_TOL * v(ko), (tag, j, kg, ko, v(kg), v(ko))
-        break
+        assert ko >= 0 and abs(v(kg) - v(ko)) <= REL_TOL * v(ko), (tag, j, kg, ko, v(kg), v(ko))
+
+
+def region_states(n, m, b=0):
+    """All states (b, j, i) of the computed region (R8): i in [j, n-m+j] for j < m, i = n for j = m."""
+    qj, qi = [], []
+    for j in range(1, m + 1):
+        lo, hi = (n, n) if (j == m and m > 1) else (j, n - m + j)
+        qj.append(np.full(hi - lo + 1, j, dtype=np.int32))
+        qi.append(np.arange(lo, hi + 1, dtype=np.int32))
+    qj, qi = np.concatenate(qj), np.concatenate(qi)
+    return np.full(qj.size, b, dtype=np.int32), qj, qi
+
+
+def query_gpu(placer, qb, qj, qi):
+    """dp values (float64, +inf for the dtype's infinity) and back-pointers of sampled states of the
+    placer's last solve, through heddle_place_query."""
+    dp, par = placer.query(to_dev(qb), to_dev(qj), to_dev(qi))
+    torch.cuda.synchronize()
+    if dp.dtype == torch.uint64:
+        v = dp.cpu().view(torch.int64).numpy().astype(np.uint64)
+        out = v.astype(np.float64)
+        out[v == np.uint64(2 ** 64 - 1)] = np.inf
+    elif dp.dtype == torch.uint32:
+        v = dp.cpu().numpy().astype(np.uint64)
+        out = v.astype(np.float64)
+        out[v == np.uint64(2 ** 32 - 1)] = np.inf
+    else:
+        out = dp.cpu().numpy().astype(np.float64)
+    return out, par.cpu().numpy()
+
+
+def assert_tables_exact(placer, b, ref, n, m, tag=""):
+    """Every dp value and back-pointer of problem b's computed region, read back through
+    heddle_place_query, equal to the oracle's tables bit for bit (U32 / F32-emulation modes)."""
+    qb, qj, qi = region_states(n, m, b)
+    dp, par = query_gpu(placer, qb, qj, qi)
+    want_dp = ref["dp"][qj, qi]
+    want_par = ref["parent"][qj, qi]
+    bad = np.nonzero((dp != want_dp) | (par != want_par))[0]
+    assert bad.size == 0, (tag, b, [(int(qj[t]), int(qi[t]), dp[t], want_dp[t], int(par[t]), int(want_par[t]))
+                                    for t in bad[:5]])

@@ -60,6 +60,28 @@ def test_spec_dp_examples():
                     assert cp["parent"][int(j), int(i)] == k
 
 
+def test_capacity_golden_cases():
+    """Hand-derived capacity cases (R6): a group whose token sum (or size) EQUALS its worker's cap
+    is admissible and is the optimum, so an off-by-one in the cap test fails here."""
+    g = json.load(open(GOLDEN))
+    for case in g["capacity"]:
+        sr = oracle.MINMAX if case["semiring"] == "minmax" else oracle.MINPLUS
+        kw = {}
+        if "kv_caps" in case:
+            kw["kvcaps"] = case["kv_caps"]
+        if "caps" in case:
+            kw["caps"] = case["caps"]
+        p = homog(case["L"], case["T"], case["F"], case["m"], mode=case["mode"], semiring=sr, **kw)
+        r = oracle.solve(p)
+        assert r["status"] == oracle.OK, case["cite"]
+        assert r["opt"] == case["opt"], (r["opt"], case["cite"])
+        assert list(r["bounds"]) == case["bounds"], (list(r["bounds"]), case["cite"])
+        bf = oracle.brute_contiguous(p)
+        assert bf["opt"] == case["opt"], case["cite"]
+        if sr == oracle.MINMAX and case["mode"] != "f64":
+            assert oracle.parametric_opt(p)["opt"] == case["opt"], case["cite"]
+
+
 def test_infeasible_n_less_than_m():
     p = homog([5, 4], 1.0, [1.0], 3)
     assert oracle.solve(p)["status"] == oracle.INFEASIBLE          # S:296
