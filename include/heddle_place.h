@@ -198,10 +198,16 @@ int64_t heddle_place_transitions(int32_t n, int32_t m);
 /* ---- multi-GPU split mode (one large instance) -------------------------
  * The columns of every DP layer are dealt to `world` ranks in zigzag order of
  * 512-column blocks (rank r owns blocks r and 2P-1-r of every group of 2P, which
- * balances the triangular work); each rank computes its blocks with the layered
- * kernel and the finished row is exchanged with one ncclAllGather per layer on the
- * solve stream.  Every rank then holds every dp row, so objective and boundaries
- * are identical on all ranks (and bit-identical to a single-GPU solve).
+ * balances the triangular work); each rank computes its blocks with the persistent
+ * layered kernel, and the tile that completes a block stores the block's final dp
+ * values straight into every peer's copy of the row over NVLink (CUDA-IPC peer memory,
+ * opened at init) and then bumps the peer's per-block ready counter (system-scope
+ * release): the exchange is fused into the DP kernel, with no NCCL call, pack or
+ * unpack on the path.  A consumer tile on any rank waits only for the blocks of row
+ * j-1 its split range covers.  HEDDLE_PLACE_EXCHANGE=nccl in the environment selects
+ * the baseline instead: one launch per layer and one ncclAllGather of the packed row.
+ * Every rank then holds every dp row, so objective and boundaries are identical on
+ * all ranks (and bit-identical to a single-GPU solve).
  * heddle_place_solve / _backtrack are collective: all ranks call them with the same
  * problem.  HEDDLE_KEEP_PARENTS is not available in split mode (E_INVALID).
  *
@@ -217,6 +223,11 @@ heddle_status heddle_place_nccl_unique_id(void* id_out, int32_t bytes);
 heddle_status heddle_place_init_split(const heddle_place_config* cfg, const void* nccl_unique_id, int32_t rank,
                                       int32_t world, heddle_place_ctx** out);
 int32_t heddle_place_split_blocks(int32_t ncb, int32_t world, int32_t rank, int32_t* blocks_out, int32_t cap);
+/* heddle_place_split_plan: host-only; per problem of an (n, m) solve, the number of (layer, block)
+ *   pieces of the dp rows that `rank` publishes to each peer (*publishes_out) and the number it
+ *   receives from the peers and waits for (*arrivals_out).  Returns 0, or -1 on bad arguments. */
+int32_t heddle_place_split_plan(int32_t n, int32_t m, int32_t world, int32_t rank, int64_t* publishes_out,
+                                int64_t* arrivals_out);
 
 /* Objective only, min-max: the exact optimum dp[m][n] of each problem, bit-identical
  * to heddle_place_solve's objective, found without the O(n^2 m) DP: bisection over the ordered

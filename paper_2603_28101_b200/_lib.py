@@ -30,7 +30,7 @@ SYMBOLS = ("heddle_place_init", "heddle_place_solve", "heddle_place_backtrack", 
            "heddle_place_solve_host",
            "heddle_place_launch_count", "heddle_place_transitions", "heddle_place_destroy",
            "heddle_place_strerror", "heddle_place_nccl_unique_id", "heddle_place_init_split",
-           "heddle_place_split_blocks", "heddle_place_debug_violations", "heddle_place_retarget",
+           "heddle_place_split_blocks", "heddle_place_split_plan", "heddle_place_debug_violations", "heddle_place_retarget",
            "heddle_place_objective")
 
 
@@ -92,6 +92,8 @@ def lib() -> ctypes.CDLL:
                                               ctypes.POINTER(vp)]
         L.heddle_place_init_split.restype = ctypes.c_int
         L.heddle_place_split_blocks.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, vp, ctypes.c_int32]
+        L.heddle_place_split_plan.argtypes = [ctypes.c_int32] * 4 + [vp, vp]
+        L.heddle_place_split_plan.restype = ctypes.c_int32
         L.heddle_place_split_blocks.restype = ctypes.c_int32
         L.heddle_place_objective.argtypes = [vp, ctypes.POINTER(Problem), vp, vp, vp]
         L.heddle_place_objective.restype = ctypes.c_int
@@ -127,6 +129,14 @@ def split_blocks(ncb: int, world: int, rank: int) -> list[int]:
     buf = (ctypes.c_int32 * max(cnt, 1))()
     lib().heddle_place_split_blocks(ncb, world, rank, buf, cnt)
     return list(buf[:cnt])
+
+
+def split_plan(n: int, m: int, world: int, rank: int) -> tuple[int, int]:
+    """(pieces this rank publishes to each peer, pieces it receives) per problem in split mode."""
+    pub, arr = ctypes.c_int64(0), ctypes.c_int64(0)
+    if lib().heddle_place_split_plan(n, m, world, rank, ctypes.byref(pub), ctypes.byref(arr)) != 0:
+        raise ValueError("heddle_place_split_plan: bad arguments")
+    return pub.value, arr.value
 
 
 def nccl_unique_id() -> bytes:

@@ -213,6 +213,26 @@ __host__ __device__ inline int owned_slots(int ncb, int world) {
   return world <= 1 ? ncb : 2 * ((ncb + 2 * world - 1) / (2 * world));
 }
 
+// Split-mode traffic per problem (host logic of the fused exchange): the blocks of layers 2..m
+// with computed columns that `rank` owns -- each is published to the world-1 peers by the tile
+// that completes it -- and the blocks owned by other ranks, whose arrival this rank waits for
+// before the backtrack.  Layer m computes only column n, so only its last block counts.
+__host__ inline void split_traffic(int n, int m, int world, int rank, int64_t* own, int64_t* foreign) {
+  const int ncb = (n - m + 3) / kK3Cols + 1;
+  *own = 0;
+  *foreign = 0;
+  for (int j = 2; j <= m; ++j) {
+    const int cbase = j & ~3, imax = n - m + j;
+    for (int blk = 0; blk < ncb; ++blk) {
+      const int c0 = cbase + kK3Cols * blk;
+      if (c0 > imax) break;
+      if (j == m && c0 + kK3Cols <= n) continue;
+      const int w = blk % (2 * world);
+      if ((w < world ? w : 2 * world - 1 - w) == rank) ++*own; else ++*foreign;
+    }
+  }
+}
+
 // pack row j of the blocks owned by `rank` into buf[b][slot][kK3Cols] (+inf padding)
 template <int DT, int SR>
 __global__ void k3_pack(SolveArgs a, int j, int rank, int world, int nown, void* buf) {

@@ -385,17 +385,8 @@ heddle_status solve_persistent(heddle_place_ctx* x, SolveArgs& a, cudaStream_t s
     pa.start_flag = x->d_flags;
     pa.wait_start = x->expect[0];
     // arrivals: one per (problem, block of layers 2..m with computed columns) owned by another rank
-    int64_t foreign = 0;
-    for (int j = 2; j <= m; ++j) {
-      const int cbase = j & ~3, imax = n - m + j;
-      for (int blk = 0; blk < ncb; ++blk) {
-        const int c0 = cbase + kK3Cols * blk;
-        if (c0 > imax) break;
-        if (j == m && c0 + kK3Cols <= n) continue;
-        const int w = blk % (2 * world);
-        if ((w < world ? w : 2 * world - 1 - w) != rank) ++foreign;
-      }
-    }
+    int64_t own = 0, foreign = 0;
+    split_traffic(n, m, world, rank, &own, &foreign);
     x->arrive_total += (unsigned long long)foreign * B;
     pa.peer_arrive = x->d_peer_arrive;
     pa.arrive = x->d_flags + x->max_m + 1;
@@ -1284,6 +1275,14 @@ heddle_status heddle_place_init_split(const heddle_place_config* cfg, const void
   }
   *out = x;
   return HEDDLE_OK;
+}
+
+int32_t heddle_place_split_plan(int32_t n, int32_t m, int32_t world, int32_t rank, int64_t* publishes_out,
+                                int64_t* arrivals_out) {
+  if (n < 1 || m < 1 || n < m || world < 1 || rank < 0 || rank >= world || !publishes_out || !arrivals_out)
+    return -1;
+  split_traffic(n, m, world, rank, publishes_out, arrivals_out);
+  return 0;
 }
 
 int32_t heddle_place_split_blocks(int32_t ncb, int32_t world, int32_t rank, int32_t* blocks_out, int32_t cap) {

@@ -71,3 +71,56 @@ def test_gather_shards_gloo_world2(B):
         p.join(timeout=120)
         assert p.exitcode == 0
     assert all(ok for _, ok in res), res
+
+
+# ------------------------------------------------------------------ split mode host logic (world 2, 3)
+def _split_worker(rank, world, port, q):
+    """One rank of the split-mode control plane: the unique-id broadcast of dist.split_placer, the
+    zigzag column ownership (heddle_place_split_blocks) and the fused exchange's per-rank publish /
+    arrival counts (heddle_place_split_plan), checked across ranks over gloo."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2603_28101_b200 import _lib as C
+    ok = True
+    obj = [C.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    ids = [None] * world
+    dist.all_gather_object(ids, obj[0])
+    ok &= len(obj[0]) == 128 and all(i == ids[0] for i in ids)
+    for n, m in ((65536, 256), (8192, 12), (4096, 64), (2100, 7), (600, 300)):
+        ncb = (n - m + 3) // 512 + 1
+        mine = C.split_blocks(ncb, world, rank)
+        owners = [None] * world
+        dist.all_gather_object(owners, mine)
+        allb = sorted(b for o in owners for b in o)
+        ok &= allb == list(range(ncb))                     # every block owned exactly once
+        # zigzag balance: the triangular work (splits below each column, summed) per rank
+        work = sum(sum(min(c, n) for c in range(512 * b, 512 * b + 512)) for b in mine)
+        works = [None] * world
+        dist.all_gather_object(works, work)
+        if ncb >= 4 * world:
+            ok &= max(works) / (sum(works) / world) < 1.0 + 2.0 * world / ncb
+        pub, arr = C.split_plan(n, m, world, rank)
+        plans = [None] * world
+        dist.all_gather_object(plans, (pub, arr))
+        total = sum(p for p, _ in plans)
+        ok &= arr == total - pub                          # every peer's publications arrive here
+        ok &= sum(a for _, a in plans) == (world - 1) * total
+    q.put((rank, bool(ok)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_split_host_logic_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_split_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert sorted(res) == [(r, True) for r in range(world)], res
