@@ -27,6 +27,9 @@ def main():
     ap.add_argument("--budget", type=int, default=64)
     ap.add_argument("--objective-only", action="store_true", help="makespans by the parametric kernel (N3)")
     ap.add_argument("--algo", default="valley", help="DP solver: valley (N3) or scan (Eq. 3 as written)")
+    ap.add_argument("--impl", default="device", choices=["device", "host"],
+                    help="device: the whole walk on the GPU (heddle_place_anneal, K9 + ragged solves, CUDA graph); "
+                         "host: moves and Metropolis in Python, one solve per distinct worker count")
     args = ap.parse_args()
     import torch
 
@@ -41,16 +44,18 @@ def main():
     iu, su = wl.sa_uniforms(11, args.chains, cfg.max_iters)
     rm = alloc.ResourceManager(prof, n_max=args.n, m_max=cfg.m_max, chains=args.chains,
                                objective_only=args.objective_only, algo=args.algo)
-    rm.anneal(L, alloc.SAConfig(budget=args.budget, m_min=8, m_max=args.budget, max_iters=3), iu, su)  # warm-up
+    run = rm.anneal if args.impl == "device" else rm.anneal_host
+    run(L, alloc.SAConfig(budget=args.budget, m_min=8, m_max=args.budget, max_iters=3), iu, su)  # warm-up
     torch.cuda.synchronize()
     rm.evaluations = 0
     t = time.perf_counter()
-    res = rm.anneal(L, cfg, iu, su)
+    res = run(L, cfg, iu, su)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t
     homog = {d: rm.makespans(torch.from_numpy(L).cuda(), [tuple([d] * (args.budget // d))])[0][0]
              for d in (1, 2, 4, 8) if args.budget // d >= 8}
-    print(json.dumps({"n": args.n, "budget": args.budget, "chains": args.chains, "iterations": res.iterations,
+    print(json.dumps({"impl": args.impl, "n": args.n, "budget": args.budget, "chains": args.chains,
+                      "iterations": res.iterations,
                       "evaluator": "parametric objective (N3)" if args.objective_only else f"DP solve ({args.algo}) + backtrack",
                       "evaluations": res.evaluations, "wall_s": dt, "dp_evals_per_s": res.evaluations / dt,
                       "best_makespan_s": res.best_makespan, "best_degrees": list(res.best_degrees),

@@ -10,7 +10,7 @@ $CS --version > gpurun_out/${tag}_sanitizer_version.txt 2>&1
 for tool in memcheck racecheck synccheck initcheck; do
   extra=""
   [ "$tool" = "racecheck" ] && extra="--racecheck-report all"
-  timeout 1500 $CS --tool $tool $extra --target-processes all --print-limit 100 \
+  timeout 700 $CS --tool $tool $extra --target-processes all --print-limit 100 \
       python tests/sanitize_run.py > gpurun_out/${tag}_sanitize_${tool}.log 2>&1
   echo "$tool exit $?" >> gpurun_out/${tag}_sanitize_summary.txt
   tail -3 gpurun_out/${tag}_sanitize_${tool}.log >> gpurun_out/${tag}_sanitize_summary.txt

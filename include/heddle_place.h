@@ -133,6 +133,14 @@ typedef struct {
                                 /*   (one-CTA-per-problem) kernel only: E_INVALID if n needs the  */
                                 /*   layered kernel                                             */
   int64_t weights_stride;
+  const int32_t* ms;            /* [B] per-problem worker count m_b in [1, m], or NULL (= m for all): a
+                                 *   ragged batch, e.g. the simulated-annealing proposals of Alg. 2
+                                 *   (P:748-753), whose split / merge moves change the worker count,
+                                 *   evaluated in ONE launch.  Problem b uses degrees[b][0..m_b) (and
+                                 *   caps / kv_caps likewise); its boundaries row holds b_0..b_{m_b}
+                                 *   followed by -1 up to index m.  One-CTA-per-problem kernels only
+                                 *   (n must fit shared memory; E_INVALID otherwise and in split mode).
+                                 *   m_b outside [1, m] gives that problem HEDDLE_E_INVALID.         */
 } heddle_place_problem;
 
 /* Creates a context on cfg->device: copies and validates the profile (E_RANGE
@@ -238,6 +246,50 @@ int32_t heddle_place_split_plan(int32_t n, int32_t m, int32_t world, int32_t ran
  * weights) and split-mode contexts.  Same per-problem status_out / +inf conventions as solve. */
 heddle_status heddle_place_objective(heddle_place_ctx* ctx, const heddle_place_problem* prob, void* objective_out,
                                      int32_t* status_out, void* stream);
+
+/* ---- device-resident resource manager: Sort-Initialized Simulated Annealing,
+ * Alg. 2, P independent chains over sorted MP-degree allocations.  Per
+ * iteration, all on `stream` with no host round trip (one CUDA graph replayed per iteration):
+ *   perturb one thread per live chain: kind = floor(3 u0), falling through split ->
+ *            merge -> redistribute when inapplicable (R13); candidates in descending
+ *            degree order picked by floor(u * count) with u1 (and u2 for the redistribute
+ *            alternative); split / merge change the worker count within [m_min, m_max] (R14);
+ *            a proposal with more workers than n keeps the current state;
+ *   evaluate ONE ragged heddle_place_solve (or heddle_place_objective when
+ *            objective_only) over the P proposals, this context's algorithm and arithmetic;
+ *   accept Metropolis: accept iff dC < 0 or u3 < exp(-dC / T); best-so-far;
+ *            T <- cooling * T; a chain stops once T <= eps_frac * T0 (T0 = its start makespan).
+ * The allowed degrees are the profile's.  Uniforms are inputs (R16): [P][iters][4] doubles
+ * (kind, first pick, second pick, acceptance).  The start states come from the caller (sorted
+ * degree rows padded to m_max, counts init_m).  One host synchronisation after the start states
+ * are evaluated (the iteration count); E_INVALID for P > 1024 or > max_batch, m_max > max_m,
+ * n > max_n, more than 16 profile degrees, cooling outside (0, 1), or split-mode contexts; the
+ * solve's own errors are returned as they are.  A following heddle_place_backtrack is E_STATE.   */
+typedef struct {
+  int32_t n;                   /* trajectories; lengths: device [n] dtype, non-increasing */
+  const void* lengths;
+  int32_t chains;              /* P, 1..1024                                                      */
+  int32_t m_min, m_max;        /* worker-count bounds; m_max is the row stride of degree rows     */
+  const int32_t* init_degrees; /* device [P][m_max] start allocation per chain, non-increasing     */
+  const int32_t* init_m;       /* device [P] workers of each start allocation                     */
+  const double* uniforms;      /* device [P][iters][4]                                             */
+  int32_t iters;               /* iteration cap (max_iters)                                        */
+  double cooling;              /* alpha of T <- alpha T                                    */
+  double eps_frac;             /* stop at T <= eps_frac * T0                                       */
+  int32_t objective_only;      /* 1: makespans by heddle_place_objective (min-max only)            */
+} heddle_place_anneal_args;
+
+typedef struct {
+  double* best_makespan;       /* device [P] best makespan per chain (as double)                   */
+  int32_t* best_degrees;       /* device [P][m_max] best allocation (padded past best_m)           */
+  int32_t* best_m;             /* device [P]                                                       */
+  double* trace;               /* device [P][iters+1] or NULL: current makespan after each iteration */
+  int32_t* accepted;           /* device [P][iters] or NULL: 1 where the iteration's move was accepted */
+  int32_t* iterations;         /* host, or NULL: iterations run (the longest chain's)              */
+} heddle_place_anneal_out;
+
+heddle_status heddle_place_anneal(heddle_place_ctx* ctx, const heddle_place_anneal_args* args,
+                                  heddle_place_anneal_out* out, void* stream);
 
 /* Migration retarget (§5.3).  For each query q: problem
  * query_problem[q] with plan boundaries[b][0..m] (from heddle_place_backtrack; n = b_m), n_active[b]

@@ -31,7 +31,7 @@ SYMBOLS = ("heddle_place_init", "heddle_place_solve", "heddle_place_backtrack", 
            "heddle_place_launch_count", "heddle_place_transitions", "heddle_place_destroy",
            "heddle_place_strerror", "heddle_place_nccl_unique_id", "heddle_place_init_split",
            "heddle_place_split_blocks", "heddle_place_split_plan", "heddle_place_debug_violations", "heddle_place_retarget",
-           "heddle_place_objective")
+           "heddle_place_objective", "heddle_place_anneal")
 
 
 class Config(ctypes.Structure):
@@ -48,7 +48,20 @@ class Problem(ctypes.Structure):
                 ("degrees", ctypes.c_void_p), ("degrees_stride", ctypes.c_int64),
                 ("caps", ctypes.c_void_p), ("caps_stride", ctypes.c_int64),
                 ("kv_caps", ctypes.c_void_p), ("kv_caps_stride", ctypes.c_int64),
-                ("weights", ctypes.c_void_p), ("weights_stride", ctypes.c_int64)]
+                ("weights", ctypes.c_void_p), ("weights_stride", ctypes.c_int64),
+                ("ms", ctypes.c_void_p)]
+
+
+class AnnealArgs(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("lengths", ctypes.c_void_p), ("chains", ctypes.c_int32),
+                ("m_min", ctypes.c_int32), ("m_max", ctypes.c_int32), ("init_degrees", ctypes.c_void_p),
+                ("init_m", ctypes.c_void_p), ("uniforms", ctypes.c_void_p), ("iters", ctypes.c_int32),
+                ("cooling", ctypes.c_double), ("eps_frac", ctypes.c_double), ("objective_only", ctypes.c_int32)]
+
+
+class AnnealOut(ctypes.Structure):
+    _fields_ = [("best_makespan", ctypes.c_void_p), ("best_degrees", ctypes.c_void_p), ("best_m", ctypes.c_void_p),
+                ("trace", ctypes.c_void_p), ("accepted", ctypes.c_void_p), ("iterations", ctypes.c_void_p)]
 
 
 class HeddleError(RuntimeError):
@@ -76,6 +89,8 @@ def lib() -> ctypes.CDLL:
         L.heddle_place_backtrack.argtypes = [vp, vp, vp, vp]
         L.heddle_place_backtrack.restype = ctypes.c_int
         L.heddle_place_query.argtypes = [vp, ctypes.c_int32, vp, vp, vp, vp, vp, vp]
+        L.heddle_place_anneal.argtypes = [vp, ctypes.POINTER(AnnealArgs), ctypes.POINTER(AnnealOut), vp]
+        L.heddle_place_anneal.restype = ctypes.c_int
         L.heddle_place_query.restype = ctypes.c_int
         L.heddle_place_solve_host.argtypes = [vp, ctypes.POINTER(Problem), vp, vp, vp, vp,
                                               ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]

@@ -1,9 +1,13 @@
 """Sort-initialised simulated annealing over per-worker MP degrees (§6.2, Alg. 2),
-with every PresortedDP evaluation running as one batched GPU solve per iteration.
+with every PresortedDP evaluation running on the GPU.
 
 Alg. 2 is one sequential chain; the GPU turns the "~120 DPs of ~42 ms each" of the paper's resource
-manager (Table) into P independent chains whose proposals are evaluated together
-(one heddle_place_solve per distinct worker count).  Host logic here is only the Metropolis walk.
+manager (Table) into P independent chains walked together.
+`ResourceManager.anneal` runs the whole walk on the device (heddle_place_anneal, kernel K9): per
+iteration a perturb kernel, ONE ragged solve of all P proposals (their worker counts differ) and a
+Metropolis kernel, captured once as a CUDA graph -- the host only draws the start states and reads
+the results.  `ResourceManager.anneal_host` is the same walk with the moves and the acceptance in
+Python (one solve per distinct worker count per iteration), kept as a reference.
 
 Readings (R13-R16; the paper names the moves but does not define them):
   * state: the sorted (descending) multiset of degrees {N_i}, sum N_i = N (budget);
@@ -176,7 +180,57 @@ class ResourceManager:
         return out
 
     def anneal(self, lengths, cfg: SAConfig, init_uniforms, step_uniforms) -> SAResult:
-        """P chains of Alg. 2; init_uniforms [P, 1 + 3 cfg.init_moves], step_uniforms [P, iters, 4]."""
+        """P chains of Alg. 2 on the device (heddle_place_anneal); same inputs and result as
+        anneal_host.  init_uniforms [P, 1 + 3 cfg.init_moves], step_uniforms [P, iters, 4]."""
+        import ctypes
+        from . import _lib as C
+        if set(cfg.degrees) != set(int(d) for d in self.placer._deg):
+            raise ValueError("SAConfig.degrees must be the profile's degrees")
+        L = lengths if isinstance(lengths, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(lengths))
+        L = L.to(self.dev).reshape(-1).contiguous()
+        n = L.shape[0]
+        P = init_uniforms.shape[0]
+        M = cfg.m_max
+        iters = min(cfg.max_iters, step_uniforms.shape[1])
+        starts = [initial_state(cfg, n, init_uniforms[c]) for c in range(P)]
+        rows = np.full((P, M), max(cfg.degrees), dtype=np.int32)
+        for c, st in enumerate(starts):
+            rows[c, :len(st)] = st
+        init_deg = torch.from_numpy(rows).to(self.dev)
+        init_m = torch.tensor([len(st) for st in starts], dtype=torch.int32, device=self.dev)
+        u = torch.from_numpy(np.ascontiguousarray(step_uniforms[:, :iters, :], dtype=np.float64)).to(self.dev)
+        best = torch.empty(P, dtype=torch.float64, device=self.dev)
+        best_deg = torch.empty((P, M), dtype=torch.int32, device=self.dev)
+        best_m = torch.empty(P, dtype=torch.int32, device=self.dev)
+        trace = torch.empty((P, iters + 1), dtype=torch.float64, device=self.dev)
+        accepted = torch.empty((P, max(iters, 1)), dtype=torch.int32, device=self.dev)
+        nit = ctypes.c_int32(0)
+        p = lambda t: ctypes.c_void_p(t.data_ptr())
+        args = C.AnnealArgs(n, p(L), P, cfg.m_min, M, p(init_deg), p(init_m), p(u), iters, cfg.cooling,
+                            cfg.eps_frac, 1 if self.objective_only else 0)
+        out = C.AnnealOut(p(best), p(best_deg), p(best_m), p(trace), p(accepted),
+                          ctypes.cast(ctypes.byref(nit), ctypes.c_void_p))
+        s = torch.cuda.current_stream(self.dev).cuda_stream
+        C.check(C.lib().heddle_place_anneal(self.placer._h, ctypes.byref(args), ctypes.byref(out),
+                                            ctypes.c_void_p(s)), "heddle_place_anneal")
+        it = nit.value
+        self.evaluations += P * (1 + it)
+        best_h, bdeg_h, bm_h = best.cpu().numpy(), best_deg.cpu().numpy(), best_m.cpu().numpy()
+        tr_h, acc_h = trace.cpu().numpy(), accepted.cpu().numpy()
+        chain_best = [(float(best_h[c]), tuple(int(d) for d in bdeg_h[c, :bm_h[c]])) for c in range(P)]
+        traces = [[float(tr_h[c, 0])] + [float(tr_h[c, t + 1]) for t in range(it) if acc_h[c, t]] for c in range(P)]
+        b = min(range(P), key=lambda c: (chain_best[c][0], c))
+        bounds = None
+        if math.isfinite(chain_best[b][0]):   # the best allocation's partition: one DP + backtrack
+            saved, self.objective_only = self.objective_only, False
+            bounds = self.makespans(L, [chain_best[b][1]])[0][1]
+            self.evaluations -= 1
+            self.objective_only = saved
+        return SAResult(chain_best[b][1], chain_best[b][0], bounds, it, self.evaluations, chain_best, traces)
+
+    def anneal_host(self, lengths, cfg: SAConfig, init_uniforms, step_uniforms) -> SAResult:
+        """P chains of Alg. 2 with the moves and the Metropolis step on the host (reference for
+        anneal); init_uniforms [P, 1 + 3 cfg.init_moves], step_uniforms [P, iters, 4]."""
         L = lengths if isinstance(lengths, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(lengths))
         L = L.to(self.dev).reshape(-1)
         n = L.shape[0]

@@ -94,14 +94,15 @@ __global__ void __launch_bounds__(32 * kK4Warps) k4_backtrack(SolveArgs a, int32
   const int lane = threadIdx.x & 31;
   const int b = blockIdx.x * kK4Warps + (threadIdx.x >> 5);
   if (b >= a.B) return;
-  const int n = a.n, m = a.m;
-  int32_t* out = bounds + (int64_t)b * (m + 1);
+  const int n = a.n, M = a.m, m = prob_m(a, b);   // M: row stride; m: this problem's workers
+  int32_t* out = bounds + (int64_t)b * (M + 1);
   if (a.status[b] != HEDDLE_OK) {
-    for (int j = lane; j <= m; j += 32) out[j] = -1;
+    for (int j = lane; j <= M; j += 32) out[j] = -1;
     return;
   }
+  for (int j = m + 1 + lane; j <= M; j += 32) out[j] = -1;   // ragged batch: unused tail
   const L* gL = reinterpret_cast<const L*>(a.lengths) + (int64_t)b * a.ls;
-  const D* gdp = reinterpret_cast<const D*>(a.dpws) + (int64_t)b * (m + 1) * (n + 1);
+  const D* gdp = reinterpret_cast<const D*>(a.dpws) + (int64_t)b * (M + 1) * (n + 1);
   const G* gtab = reinterpret_cast<const G*>(a.gtab);
   const S* gSp = KV ? reinterpret_cast<const S*>(a.spws) + (int64_t)b * (n + 1) : nullptr;
   const int32_t* gWp = W ? a.wpws + (int64_t)b * (n + 1) : nullptr;
@@ -124,7 +125,7 @@ __global__ void __launch_bounds__(32 * kK4Warps) k4_backtrack(SolveArgs a, int32
       if (msk) found = base + __ffs(msk) - 1;
     }
     if (found < 0) {   // unreachable: the target is one of these candidates
-      for (int q = lane; q <= m; q += 32) out[q] = -1;
+      for (int q = lane; q <= M; q += 32) out[q] = -1;
       return;
     }
     cur = found;
@@ -147,15 +148,16 @@ __global__ void __launch_bounds__(kK4CtaThreads) k4_backtrack_cta(SolveArgs a, i
   using S = typename SpT<DT>::type;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int b = blockIdx.x;
-  const int n = a.n, m = a.m;
-  int32_t* out = bounds + (int64_t)b * (m + 1);
+  const int n = a.n, M = a.m, m = prob_m(a, b);
+  int32_t* out = bounds + (int64_t)b * (M + 1);
   if (a.status[b] != HEDDLE_OK) {
-    for (int j = tid; j <= m; j += kK4CtaThreads) out[j] = -1;
+    for (int j = tid; j <= M; j += kK4CtaThreads) out[j] = -1;
     return;
   }
+  for (int j = m + 1 + tid; j <= M; j += kK4CtaThreads) out[j] = -1;
   __shared__ int s_lo, s_found, s_row;
   const L* gL = reinterpret_cast<const L*>(a.lengths) + (int64_t)b * a.ls;
-  const D* gdp = reinterpret_cast<const D*>(a.dpws) + (int64_t)b * (m + 1) * (n + 1);
+  const D* gdp = reinterpret_cast<const D*>(a.dpws) + (int64_t)b * (M + 1) * (n + 1);
   const G* gtab = reinterpret_cast<const G*>(a.gtab);
   const S* gSp = KV ? reinterpret_cast<const S*>(a.spws) + (int64_t)b * (n + 1) : nullptr;
   const int32_t* gWp = W ? a.wpws + (int64_t)b * (n + 1) : nullptr;
@@ -193,7 +195,7 @@ __global__ void __launch_bounds__(kK4CtaThreads) k4_backtrack_cta(SolveArgs a, i
     const int found = s_found;
     __syncthreads();
     if (found == INT_MAX) {   // unreachable: the target is one of these candidates
-      for (int q = tid; q <= m; q += kK4CtaThreads) out[q] = -1;
+      for (int q = tid; q <= M; q += kK4CtaThreads) out[q] = -1;
       return;
     }
     cur = found;
@@ -221,14 +223,15 @@ __global__ void __launch_bounds__(32 * kK4Warps) k4_query(SolveArgs a, int nq, c
   const int lane = threadIdx.x & 31;
   const int q = blockIdx.x * kK4Warps + (threadIdx.x >> 5);
   if (q >= nq) return;
-  const int n = a.n, m = a.m;
+  const int n = a.n, M = a.m;
   const int b = qb[q], j = qj[q], cur = qi[q];
+  const int m = (b >= 0 && b < a.B) ? prob_m(a, b) : 0;
   D val = T::inf();
   int found = -1;
   const bool ok = b >= 0 && b < a.B && j >= 1 && j <= m && cur >= j && cur <= n - m + j &&
                   (j < m || cur == n || m == 1) && a.status[b] == HEDDLE_OK;
   if (ok) {
-    const D* gdp = reinterpret_cast<const D*>(a.dpws) + (int64_t)b * (m + 1) * (n + 1);
+    const D* gdp = reinterpret_cast<const D*>(a.dpws) + (int64_t)b * (M + 1) * (n + 1);
     val = T::norm(gdp[(int64_t)j * (n + 1) + cur]);
     if (val != T::inf()) {
       if (j == 1) {

@@ -79,7 +79,12 @@ struct SolveArgs {
   int ready_chunk;
   int vscan;               // valley kernel: descent prefixes shorter than this are scanned (K8)
   int2* rowcap;            // [B][m] {profile row, cap} per worker, written by the K3/K5 prologue, or null
+  const int32_t* ms;       // [B] per-problem worker count (ragged m, <= m) or null (= m); one-CTA kernels
 };
+
+// worker count of problem b (ragged batches: SA proposals of different sizes in one launch);
+// m stays the row stride of degrees / caps / boundaries and of the dp workspace
+__device__ __forceinline__ int prob_m(const SolveArgs& a, int b) { return a.ms ? __ldg(a.ms + b) : a.m; }
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
@@ -321,14 +326,14 @@ __device__ __forceinline__ void sweep_weighted(const typename Tr<DT, SR>::L* __r
 // weight prefix sums (also written to the workspace for the backtrack).  Returns the problem's
 // status; a non-zero status is already recorded (status, objective) and the CTA must return.
 template <int DT, int SR, bool KV, bool W, int NT>
-__device__ __forceinline__ int load_problem(const SolveArgs& a, int b, typename Tr<DT, SR>::L* sL, int* srow,
+__device__ __forceinline__ int load_problem(const SolveArgs& a, int b, int m, typename Tr<DT, SR>::L* sL, int* srow,
                                             int* scap, int64_t* skv, typename SpT<DT>::type* sSp, int* sWp,
                                             int& s_err) {
   using T = Tr<DT, SR>;
   using L = typename T::L;
   using D = typename T::D;
   using S = typename SpT<DT>::type;
-  const int n = a.n, m = a.m, tid = threadIdx.x;
+  const int n = a.n, tid = threadIdx.x;   // m: this problem's worker count (prob_m)
   const L* gL = reinterpret_cast<const L*>(a.lengths) + (int64_t)b * a.ls;
   // ---------------- load + validate (lengths sorted/finite/positive, degrees known and sorted)
   if (tid == 0) {
@@ -352,12 +357,12 @@ __device__ __forceinline__ int load_problem(const SolveArgs& a, int b, typename 
     if (bad_range) atomicMin(&s_err, (int)HEDDLE_E_RANGE);
     else if (t + 1 < n && sL[t + 1] > x) atomicMin(&s_err, (int)HEDDLE_E_UNSORTED);
   }
-  for (int j = tid; j < m; j += NT) {
+  for (int j = tid; j < min(m, a.m); j += NT) {
     const int d = __ldcg(a.degrees + (int64_t)b * a.ds + j);
     int row = -1;
     for (int q = 0; q < a.D; ++q) row = (a.prof_deg[q] == d) ? q : row;
     if (row < 0) atomicMin(&s_err, (int)HEDDLE_E_UNKNOWN_DEGREE);
-    if (j + 1 < m && __ldcg(a.degrees + (int64_t)b * a.ds + j + 1) > d) atomicMin(&s_err, (int)HEDDLE_E_UNSORTED);
+    if (j + 1 < min(m, a.m) && __ldcg(a.degrees + (int64_t)b * a.ds + j + 1) > d) atomicMin(&s_err, (int)HEDDLE_E_UNSORTED);
     srow[j] = row < 0 ? 0 : row;
     scap[j] = a.caps ? __ldcg(a.caps + (int64_t)b * a.cs + j) : -1;
     skv[j] = KV ? __ldcg(a.kv + (int64_t)b * a.kvs + j) : -1;
@@ -379,6 +384,7 @@ __device__ __forceinline__ int load_problem(const SolveArgs& a, int b, typename 
   }
   __syncthreads();
   int err = s_err == INT_MAX ? 0 : s_err;
+  if (m < 1 || m > a.m) err = HEDDLE_E_INVALID;        // ragged worker count outside [1, m]
   if (err == 0 && n < m) err = HEDDLE_E_INFEASIBLE;
   if (err != 0) {
     if (tid == 0) {
@@ -424,9 +430,10 @@ __global__ void __launch_bounds__(kK2Threads, (SR == HEDDLE_MINMAX && DT != HEDD
   using D = typename T::D;
   using S = typename SpT<DT>::type;
   extern __shared__ __align__(16) unsigned char smem[];
-  const int n = a.n, m = a.m, b = blockIdx.x;
+  const int n = a.n, M = a.m, b = blockIdx.x;   // M: row stride (max workers); m: this problem's
+  const int m = prob_m(a, b);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const K2Smem<DT, SR> lay(n, m, KV, W);
+  const K2Smem<DT, SR> lay(n, M, KV, W);
   G* sG = reinterpret_cast<G*>(smem + lay.gOff);
   G* sG2 = reinterpret_cast<G*>(smem + lay.g2Off);
   L* sL = reinterpret_cast<L*>(smem + lay.lOff);
@@ -442,11 +449,11 @@ __global__ void __launch_bounds__(kK2Threads, (SR == HEDDLE_MINMAX && DT != HEDD
   __shared__ D s_redv[kK2Warps];
   __shared__ int s_redk[kK2Warps];
 
-  D* gdp = reinterpret_cast<D*>(a.dpws) + (int64_t)b * (m + 1) * (n + 1);
-  int32_t* gpar = KP ? a.parws + (int64_t)b * (m + 1) * (n + 1) : nullptr;
+  D* gdp = reinterpret_cast<D*>(a.dpws) + (int64_t)b * (M + 1) * (n + 1);
+  int32_t* gpar = KP ? a.parws + (int64_t)b * (M + 1) * (n + 1) : nullptr;
   const G* gtab = reinterpret_cast<const G*>(a.gtab);
 
-  if (load_problem<DT, SR, KV, W, kK2Threads>(a, b, sL, srow, scap, skv, sSp, sWp, s_err) != 0) return;
+  if (load_problem<DT, SR, KV, W, kK2Threads>(a, b, m, sL, srow, scap, skv, sSp, sWp, s_err) != 0) return;
   for (int t = tid; t < align4(n + kLPad); t += kK2Threads) { sdp0[t] = T::inf(); sdp1[t] = T::inf(); }
 
   // ---------------- layers

@@ -15,6 +15,7 @@
 #include <vector>
 #include <algorithm>
 
+#include "anneal.cuh"
 #include "backtrack.cuh"
 #include "dp_batched.cuh"
 #include "dp_layered.cuh"
@@ -120,6 +121,11 @@ struct heddle_place_ctx {
   unsigned long long arrive_total = 0;        // cumulative K5 arrivals expected (split mode)
   unsigned long long** d_peer_arrive = nullptr; // device array [world]: &peer_flags[r][max_m + 1]
   std::vector<unsigned long long> expect;     // cumulative arrivals expected per counter
+  // device-resident annealer (K9, heddle_place_anneal): chain state, proposals, solver outputs
+  void* d_sa = nullptr;
+  size_t sa_bytes = 0;
+  cudaStream_t sa_stream = nullptr;           // capture stream of the per-iteration CUDA graph
+  std::vector<int> prof_degrees;              // host copy of the profile's degrees
 };
 
 namespace {
@@ -672,6 +678,8 @@ void heddle_place_destroy(heddle_place_ctx* ctx) {
   cudaFree(ctx->d_sp);
   cudaFree(ctx->d_status);
   cudaFree(ctx->d_stage);
+  cudaFree(ctx->d_sa);
+  if (ctx->sa_stream) cudaStreamDestroy(ctx->sa_stream);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->copy_done) cudaEventDestroy(ctx->copy_done);
   cudaFree(ctx->d_chunk_ready);
@@ -757,6 +765,7 @@ heddle_status heddle_place_init(const heddle_place_config* c, heddle_place_ctx**
   x->max_m = c->max_m;
   x->max_batch = c->max_batch;
   x->D = c->num_degrees;
+  x->prof_degrees.assign(c->degrees, c->degrees + c->num_degrees);
   x->s_max = c->s_max;
   x->flags = c->flags;
   x->gstride = c->max_n + 1;
@@ -907,7 +916,8 @@ static heddle_status solve_impl(heddle_place_ctx* x, const heddle_place_problem*
   const int smem2 = valley ? k8_smem(x->dtype, p->n, p->m, kv, wt) : k2_smem(x->dtype, x->semiring, p->n, p->m, kv, wt);
   const bool fits = smem2 <= (valley ? x->k8_smem_max : x->k2_smem_max);
   const bool wide = (x->dtype == HEDDLE_F64) || (x->dtype == HEDDLE_U32 && x->semiring == HEDDLE_MINPLUS);
-  const bool layered = !per_problem_kernel(x, p->n, p->m, p->B, kv, wt);
+  const bool ragged = p->ms != nullptr;   // per-problem worker counts: one-CTA-per-problem kernels only
+  const bool layered = !ragged && !per_problem_kernel(x, p->n, p->m, p->B, kv, wt);
   if (!layered && !fits) return HEDDLE_E_INVALID;   // n too large for the one-CTA-per-problem kernel
   if (layered && kp && wide && !valley) return HEDDLE_E_INVALID;   // packed (value, split) atomics: 32-bit values
   if (x->split_world > 1 && (!layered || kp)) return HEDDLE_E_INVALID;  // split mode: layered, no parent table
@@ -926,6 +936,7 @@ static heddle_status solve_impl(heddle_place_ctx* x, const heddle_place_problem*
   a.kvs = p->kv_caps_stride;
   a.w = p->weights;
   a.ws = p->weights_stride;
+  a.ms = p->ms;
   if (wt && !x->d_wp) {
     if (cudaMalloc(&x->d_wp, 4 * (size_t)x->max_batch * (x->max_n + 1)) != cudaSuccess) { cudaGetLastError(); return HEDDLE_E_NOMEM; }
   }
@@ -1034,9 +1045,9 @@ heddle_status heddle_place_solve_host(heddle_place_ctx* x, const heddle_place_pr
   const int64_t wrows = p.weights ? (p.weights_stride == 0 ? 1 : B) : 0;
   auto al = [](size_t v) { return (v + 255) & ~(size_t)255; };
   const size_t bl = al(es * lrows * n), bd = al(4 * drows * m), bc = al(4 * crows * m), bk = al(8 * krows * m);
-  const size_t bw = al(4 * wrows * n);
+  const size_t bw = al(4 * wrows * n), bm = p.ms ? al(4 * B) : 0;
   const size_t bo = al(8 * B), bb = al(4 * B * (m + 1)), bs = al(4 * B);
-  const size_t need = bl + bd + bc + bk + bo + bb + bs + bw;
+  const size_t need = bl + bd + bc + bk + bo + bb + bs + bw + bm;
   if (need > x->stage_bytes) {
     cudaFree(x->d_stage);
     x->d_stage = nullptr;
@@ -1047,6 +1058,7 @@ heddle_status heddle_place_solve_host(heddle_place_ctx* x, const heddle_place_pr
   char* base = static_cast<char*>(x->d_stage);
   char *dl = base, *dd = dl + bl, *dc = dd + bd, *dk = dc + bc, *dob = dk + bk, *dbd = dob + bo, *dst = dbd + bb;
   char* dw = dst + bs;
+  char* dms = dw + bw;
   int64_t h2d = 0, d2h = 0;
   // Pipelined inputs (batched kernel, many problems): the host->device copies run on a copy stream
   // in chunks of problems, each chunk followed by a 4-byte copy of the call's epoch into its ready
@@ -1054,7 +1066,7 @@ heddle_status heddle_place_solve_host(heddle_place_ctx* x, const heddle_place_pr
   // acquire poll) for its problem's chunk, so only the first chunk's copy is exposed.  Copies run on
   // the copy engines, never on the SMs the waiting CTAs hold, so the wait always ends.
   const bool kv = p.kv_caps != nullptr, wt = p.weights != nullptr;
-  const bool batched_path = per_problem_kernel(x, p.n, p.m, p.B, kv, wt);
+  const bool batched_path = p.ms != nullptr || per_problem_kernel(x, p.n, p.m, p.B, kv, wt);
   int64_t chunk = std::max<int64_t>(kPipeMinChunk, (B + kPipeChunks - 1) / kPipeChunks);
   if (const char* e = std::getenv("HEDDLE_PLACE_HOST_CHUNK")) chunk = std::max(1, std::atoi(e));   // tuning
   const int64_t chunks = batched_path ? (B + chunk - 1) / chunk : 1;
@@ -1100,7 +1112,8 @@ heddle_status heddle_place_solve_host(heddle_place_ctx* x, const heddle_place_pr
         !up(dd, p.degrees, drows, m, p.degrees_stride, 4, b0, b1) ||
         !up(dc, p.caps, crows, m, p.caps_stride, 4, b0, b1) ||
         !up(dk, p.kv_caps, krows, m, p.kv_caps_stride, 8, b0, b1) ||
-        !up(dw, p.weights, wrows, n, p.weights_stride, 4, b0, b1))
+        !up(dw, p.weights, wrows, n, p.weights_stride, 4, b0, b1) ||
+        !up(dms, p.ms, p.ms ? B : 0, 1, 1, 4, b0, b1))
       return HEDDLE_E_CUDA;
     if (pipe && cudaMemcpyAsync(x->d_chunk_ready + c, x->h_epoch, 4, cudaMemcpyHostToDevice, cs) != cudaSuccess)
       return HEDDLE_E_CUDA;
@@ -1117,6 +1130,7 @@ heddle_status heddle_place_solve_host(heddle_place_ctx* x, const heddle_place_pr
   q.kv_caps_stride = p.kv_caps_stride == 0 ? 0 : m;
   q.weights = p.weights ? reinterpret_cast<const int32_t*>(dw) : nullptr;
   q.weights_stride = p.weights_stride == 0 ? 0 : n;
+  q.ms = p.ms ? reinterpret_cast<const int32_t*>(dms) : nullptr;
   heddle_status st =
       solve_impl(x, &q, dob, reinterpret_cast<int32_t*>(dst), stream, pipe ? x->d_chunk_ready : nullptr, epoch, (int)chunk);
   if (st != HEDDLE_OK) {
@@ -1345,6 +1359,7 @@ heddle_status heddle_place_objective(heddle_place_ctx* x, const heddle_place_pro
   a.cs = p->caps_stride;
   a.kv = p->kv_caps;
   a.kvs = p->kv_caps_stride;
+  a.ms = p->ms;
   a.gtab = x->d_gtab;
   a.gstride = x->gstride;
   a.prof_deg = x->d_prof_deg;
@@ -1375,6 +1390,138 @@ heddle_status heddle_place_objective(heddle_place_ctx* x, const heddle_place_pro
 #undef HP_K7
   x->launches++;
   x->solved = false;   // no dp rows: a following backtrack is a state error
+  return cudaGetLastError() == cudaSuccess ? HEDDLE_OK : HEDDLE_E_CUDA;
+}
+
+heddle_status heddle_place_anneal(heddle_place_ctx* x, const heddle_place_anneal_args* A, heddle_place_anneal_out* O,
+                                  void* stream) {
+  if (!x || !A || !O || !A->lengths || !A->init_degrees || !A->init_m || !A->uniforms || !O->best_makespan ||
+      !O->best_degrees || !O->best_m)
+    return HEDDLE_E_INVALID;
+  const int P = A->chains, M = A->m_max, n = A->n;
+  if (P < 1 || P > 1024 || P > x->max_batch || M < 1 || M > x->max_m || n < 1 || n > x->max_n || A->m_min < 1 ||
+      A->m_min > M || A->iters < 0 || x->D > kK9MaxD || x->split_world > 1 || !(A->cooling > 0.0 && A->cooling < 1.0))
+    return HEDDLE_E_INVALID;
+  DeviceGuard guard(x->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // workspace: degree rows (cur, prop), counters, per-chain doubles, the solver's objective / status
+  auto al = [](size_t v) { return (v + 255) & ~(size_t)255; };
+  const size_t rows = al(4 * (size_t)P * M), ints = al(4 * (size_t)P), dbl = al(8 * (size_t)P);
+  const size_t need = 2 * rows + 3 * ints + 3 * dbl + al(4) + al(8 * (size_t)P) + ints + al(4 * (size_t)x->D);
+  if (need > x->sa_bytes) {
+    cudaFree(x->d_sa);
+    x->d_sa = nullptr;
+    x->sa_bytes = 0;
+    if (cudaMalloc(&x->d_sa, need) != cudaSuccess) { cudaGetLastError(); return HEDDLE_E_NOMEM; }
+    x->sa_bytes = need;
+  }
+  if (!x->sa_stream && cudaStreamCreateWithFlags(&x->sa_stream, cudaStreamNonBlocking) != cudaSuccess)
+    return HEDDLE_E_CUDA;
+  char* w = static_cast<char*>(x->d_sa);
+  AnnealArgs sa{};
+  sa.P = P; sa.M = M; sa.n = n; sa.D = x->D;
+  sa.m_min = A->m_min; sa.m_max = M;
+  sa.u = A->uniforms; sa.iters = A->iters; sa.cooling = A->cooling;
+  sa.cur_deg = reinterpret_cast<int*>(w); w += rows;
+  sa.prop_deg = reinterpret_cast<int*>(w); w += rows;
+  sa.cur_m = reinterpret_cast<int*>(w); w += ints;
+  sa.prop_m = reinterpret_cast<int*>(w); w += ints;
+  sa.live = reinterpret_cast<int*>(w); w += ints;
+  sa.C = reinterpret_cast<double*>(w); w += dbl;
+  sa.T = reinterpret_cast<double*>(w); w += dbl;
+  sa.eps = reinterpret_cast<double*>(w); w += dbl;
+  sa.it = reinterpret_cast<int*>(w); w += al(4);
+  void* obj = w; w += al(8 * (size_t)P);
+  int32_t* st = reinterpret_cast<int32_t*>(w); w += ints;
+  int* deg_desc = reinterpret_cast<int*>(w);
+  sa.deg_desc = deg_desc;
+  sa.best = static_cast<double*>(O->best_makespan);
+  sa.best_deg = O->best_degrees;
+  sa.best_m = O->best_m;
+  sa.trace_c = O->trace;
+  sa.accepted = O->accepted;
+  sa.obj = obj;
+  sa.obj_kind = x->dtype == HEDDLE_F32 ? 0 : x->dtype == HEDDLE_F64 ? 1 : (x->semiring == HEDDLE_MINPLUS ? 3 : 2);
+  std::vector<int> hdeg(x->prof_degrees);
+  std::sort(hdeg.begin(), hdeg.end(), std::greater<int>());
+  if (cudaMemcpyAsync(deg_desc, hdeg.data(), 4 * hdeg.size(), cudaMemcpyHostToDevice, s) != cudaSuccess ||
+      cudaMemcpyAsync(sa.cur_deg, A->init_degrees, 4 * (size_t)P * M, cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
+      cudaMemcpyAsync(sa.cur_m, A->init_m, 4 * (size_t)P, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+    return HEDDLE_E_CUDA;
+  if (cudaStreamSynchronize(s) != cudaSuccess) return HEDDLE_E_CUDA;   // hdeg is a host temporary
+  // the PresortedDP makespans of one ragged batch of allocations (rows of `deg`, counts `ms`)
+  auto evaluate = [&](const int* deg, const int* ms, cudaStream_t q) -> heddle_status {
+    heddle_place_problem pb{};
+    pb.n = n; pb.m = M; pb.B = P;
+    pb.lengths = A->lengths; pb.lengths_stride = 0;
+    pb.degrees = deg; pb.degrees_stride = M;
+    pb.ms = ms;
+    return A->objective_only ? heddle_place_objective(x, &pb, obj, st, q) : heddle_place_solve(x, &pb, obj, st, q);
+  };
+  // lines 1-4: the start states' makespans, T0, eps, best
+  heddle_status e = evaluate(sa.cur_deg, sa.cur_m, s);
+  if (e != HEDDLE_OK) return e;
+  k9_start<<<(P + 127) / 128, 128, 0, s>>>(sa, A->eps_frac);
+  x->launches++;
+  // iteration count: every chain cools from its own T0 by the same factor and stops at
+  // eps_frac * T0; replay the host arithmetic of the walk to find the last live iteration
+  std::vector<double> hC(P);
+  if (cudaMemcpyAsync(hC.data(), sa.C, 8 * (size_t)P, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return HEDDLE_E_CUDA;
+  int nit = 0;
+  for (int c = 0; c < P; ++c) {
+    double T = hC[c];
+    const double eps = A->eps_frac * hC[c];
+    int k = 0;
+    while (T > eps && k < A->iters) { T *= A->cooling; ++k; }
+    nit = std::max(nit, k);
+  }
+  // lines 5-16: perturb -> ragged solve -> accept, captured once as a CUDA graph and replayed
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  bool graphed = false;
+  if (nit > 1) {
+    cudaEvent_t ev;
+    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess) {
+      cudaEventRecord(ev, s);
+      cudaStreamWaitEvent(x->sa_stream, ev, 0);
+      cudaEventDestroy(ev);
+    }
+    const int64_t l0 = x->launches;
+    if (cudaStreamBeginCapture(x->sa_stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+      k9_perturb<<<(P + 127) / 128, 128, 0, x->sa_stream>>>(sa);
+      const heddle_status ge = evaluate(sa.prop_deg, sa.prop_m, x->sa_stream);
+      k9_accept<<<1, ((P + 31) / 32) * 32, 0, x->sa_stream>>>(sa);
+      const cudaError_t ce = cudaStreamEndCapture(x->sa_stream, &graph);
+      graphed = ge == HEDDLE_OK && ce == cudaSuccess && graph &&
+                cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
+    }
+    cudaGetLastError();
+    x->launches = l0;
+    if (!graphed) {
+      if (exec) cudaGraphExecDestroy(exec);
+      exec = nullptr;
+    }
+  }
+  for (int it = 0; it < nit; ++it) {
+    if (graphed) {
+      if (cudaGraphLaunch(exec, s) != cudaSuccess) { e = HEDDLE_E_CUDA; break; }
+      x->launches += 3;
+    } else {
+      k9_perturb<<<(P + 127) / 128, 128, 0, s>>>(sa);
+      x->launches++;
+      e = evaluate(sa.prop_deg, sa.prop_m, s);
+      if (e != HEDDLE_OK) break;
+      k9_accept<<<1, ((P + 31) / 32) * 32, 0, s>>>(sa);
+      x->launches++;
+    }
+  }
+  if (exec) cudaGraphExecDestroy(exec);
+  if (graph) cudaGraphDestroy(graph);
+  if (e != HEDDLE_OK) return e;
+  x->solved = false;   // the workspace holds the last proposals' rows, not a caller's solve
+  if (O->iterations) *O->iterations = nit;
   return cudaGetLastError() == cudaSuccess ? HEDDLE_OK : HEDDLE_E_CUDA;
 }
 

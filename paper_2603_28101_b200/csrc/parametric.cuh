@@ -105,7 +105,8 @@ __global__ void __launch_bounds__(WPP == 1 ? 32 * kK7Warps : 32 * WPP) k7_parame
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int b = WPP == 1 ? (int)(blockIdx.x * kK7Warps + warp) : (int)blockIdx.x;
   if (b >= a.B) return;
-  const int n = a.n, m = a.m;
+  const int n = a.n, m0 = prob_m(a, b);   // ragged batches: this problem's worker count
+  const int m = min(max(m0, 1), a.m);
   const L* gL = reinterpret_cast<const L*>(a.lengths) + (int64_t)b * a.ls;
   __shared__ int s_err;
   __shared__ unsigned s_feas[WPP == 1 ? 1 : WPP];
@@ -130,6 +131,7 @@ __global__ void __launch_bounds__(WPP == 1 ? 32 * kK7Warps : 32 * WPP) k7_parame
     }
     err = __reduce_min_sync(0xffffffffu, err ? err : INT_MAX);
     err = err == INT_MAX ? 0 : err;
+    if (m0 != m) err = HEDDLE_E_INVALID;
     if (err == 0 && n < m) err = HEDDLE_E_INFEASIBLE;
   }
   S* gSp = KV ? reinterpret_cast<S*>(a.spws) + (int64_t)b * (n + 1) : nullptr;

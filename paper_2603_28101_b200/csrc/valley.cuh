@@ -242,8 +242,9 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k8_valley(SolveArgs a) {
   using D = typename T::D;
   using S = typename SpT<DT>::type;
   extern __shared__ __align__(16) unsigned char smem[];
-  const int n = a.n, m = a.m, b = blockIdx.x, tid = threadIdx.x;
-  const K8Smem<DT> lay(n, m, KV, W);
+  const int n = a.n, M = a.m, b = blockIdx.x, tid = threadIdx.x;   // M: row stride; m: this problem's
+  const int m = prob_m(a, b);
+  const K8Smem<DT> lay(n, M, KV, W);
   L* sL = reinterpret_cast<L*>(smem + lay.lOff);
   G* sG = W ? nullptr : reinterpret_cast<G*>(smem + lay.gOff);
   D* const sdp0 = reinterpret_cast<D*>(smem + lay.d0Off);
@@ -258,10 +259,10 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k8_valley(SolveArgs a) {
   int64_t* skv = reinterpret_cast<int64_t*>(smem + lay.kvOff);
   __shared__ int s_err, s_dlast[2];
   if (tid == 0) { s_dlast[0] = -1; s_dlast[1] = -1; }
-  if (load_problem<DT, HEDDLE_MINMAX, KV, W, NT>(a, b, sL, srow, scap, skv, sSp, sWp, s_err) != 0) return;
+  if (load_problem<DT, HEDDLE_MINMAX, KV, W, NT>(a, b, m, sL, srow, scap, skv, sSp, sWp, s_err) != 0) return;
   __syncthreads();
-  D* gdp = reinterpret_cast<D*>(a.dpws) + (int64_t)b * (m + 1) * (n + 1);
-  int32_t* gpar = KP ? a.parws + (int64_t)b * (m + 1) * (n + 1) : nullptr;
+  D* gdp = reinterpret_cast<D*>(a.dpws) + (int64_t)b * (M + 1) * (n + 1);
+  int32_t* gpar = KP ? a.parws + (int64_t)b * (M + 1) * (n + 1) : nullptr;
   const G* gtab = reinterpret_cast<const G*>(a.gtab);
   const int nb = vblocks(n);
 

@@ -374,7 +374,7 @@ def test_sa_gpu_matches_oracle_sa():
     cfg = alloc.SAConfig(budget=48, m_min=2, m_max=40, max_iters=90)
     iu, su = wl.sa_uniforms(3, 6, 90)
     rm = alloc.ResourceManager(prof, n_max=256, m_max=40, chains=6)
-    res = rm.anneal(L, cfg, iu, su)
+    res = rm.anneal_host(L, cfg, iu, su)
     c, N, chains = osa.anneal(L.astype(np.float64), prof.T, prof.F, prof.degrees, 48, iu, su, m_min=2, m_max=40,
                               max_iters=90)
     assert res.best_makespan == c and res.best_degrees == N
@@ -384,12 +384,12 @@ def test_sa_gpu_matches_oracle_sa():
     assert np.array_equal(res.best_boundaries, ref["bounds"])
     # the same walk with the exact objective-only (parametric, N3) evaluator
     rm2 = alloc.ResourceManager(prof, n_max=256, m_max=40, chains=6, objective_only=True)
-    res2 = rm2.anneal(L, cfg, iu, su)
+    res2 = rm2.anneal_host(L, cfg, iu, su)
     assert res2.best_makespan == c and res2.best_degrees == N and res2.trace == res.trace
     assert np.array_equal(res2.best_boundaries, ref["bounds"])
     # and with the full scan as the DP solver (the default is the valley search)
     rm3 = alloc.ResourceManager(prof, n_max=256, m_max=40, chains=6, algo="scan")
-    res3 = rm3.anneal(L, cfg, iu, su)
+    res3 = rm3.anneal_host(L, cfg, iu, su)
     assert res3.best_makespan == c and res3.best_degrees == N and res3.trace == res.trace
     assert np.array_equal(res3.best_boundaries, ref["bounds"])
 
