@@ -778,10 +778,22 @@ __global__ void __launch_bounds__(kK3Threads, sizeof(typename Tr<DT, SR>::D) == 
         const int64_t roff = ((int64_t)b * (m + 1) + j) * (n + 1);
         const D* mine = reinterpret_cast<const D*>(a.dpws) + roff;
         const int lo = max(c0, j), hi = imaxb;
-        for (int r = 0; r < pa.own_world; ++r) {
-          if (r == pa.own_rank) continue;
-          D* dst = reinterpret_cast<D*>(pa.peer_dp[r]) + roff;
-          for (int i = lo + tid; i <= hi; i += kK3Threads) dst[i] = ld_cg(mine + i);
+        // 16-byte chunks (each loaded once, stored to every peer) between scalar head and tail;
+        // the peers' workspaces are cudaMalloc'd like this one, so offsets align alike
+        constexpr int PER = 16 / (int)sizeof(D);
+        const int head = min(hi + 1 - lo, (int)((PER - (roff + lo) % PER) % PER));
+        const int nvec = (hi + 1 - lo - head) / PER;
+        const int vlo = lo + head, tlo = vlo + nvec * PER;
+        for (int v = tid; v < nvec; v += kK3Threads) {
+          const int4 x = __ldcg(reinterpret_cast<const int4*>(mine + vlo) + v);
+          for (int r = 0; r < pa.own_world; ++r)
+            if (r != pa.own_rank) reinterpret_cast<int4*>(reinterpret_cast<D*>(pa.peer_dp[r]) + roff + vlo)[v] = x;
+        }
+        for (int i = tid; i < head + (hi + 1 - tlo); i += kK3Threads) {
+          const int e = i < head ? lo + i : tlo + (i - head);
+          const D x = ld_cg(mine + e);
+          for (int r = 0; r < pa.own_world; ++r)
+            if (r != pa.own_rank) reinterpret_cast<D*>(pa.peer_dp[r])[roff + e] = x;
         }
         __threadfence_system();
         __syncthreads();
