@@ -155,6 +155,26 @@ class ClockSampler:
                 "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+def nvlink_kib(dev_index):
+    """NVML NVLink data counters of this GPU, summed over its links: (tx KiB, rx KiB), or None.
+    (NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX / _RX = 138 / 139; scopeId = link, values in KiB.)"""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+        tx = rx = 0
+        ok = False
+        for link in range(18):
+            vals = pynvml.nvmlDeviceGetFieldValues(h, [(138, link), (139, link)])
+            if vals[0].nvmlReturn == 0 and vals[1].nvmlReturn == 0:
+                tx += vals[0].value.ullVal
+                rx += vals[1].value.ullVal
+                ok = True
+        return (tx, rx) if ok else None
+    except Exception:
+        return None
+
+
 def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
@@ -343,6 +363,7 @@ def run_cuda(args):
     torch.cuda.synchronize()
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     launches0 = placer.launches
+    nvl0 = nvlink_kib(local) if world > 1 else None
     with ClockSampler(local) as clk:
         for s in range(args.steps):
             flush.fill_(float(s))                      # L2 flush between timed iterations (not timed)
@@ -356,6 +377,9 @@ def run_cuda(args):
             ev[s][2].record(stream)
         torch.cuda.synchronize()
     launches = placer.launches - launches0
+    nvl1 = nvlink_kib(local) if nvl0 is not None else None
+    nvl = None if (nvl0 is None or nvl1 is None) else [(nvl1[0] - nvl0[0]) * 1024.0 / args.steps,
+                                                         (nvl1[1] - nvl0[1]) * 1024.0 / args.steps]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -404,6 +428,12 @@ def run_cuda(args):
 
     vals = torch.tensor([t_step, t_k2, t_e2e, float(launches), t_valley, 0.0 if same else 1.0],
                         dtype=torch.float64, device=dev)
+    nvl_all = None
+    if world > 1:   # NVLink bytes each rank sent / received per step (NVML counters around the timed steps)
+        nv = torch.tensor(nvl if nvl is not None else [-1.0, -1.0], dtype=torch.float64, device=dev)
+        gathered = [torch.empty_like(nv) for _ in range(world)]
+        dist.all_gather(gathered, nv)
+        nvl_all = [g.tolist() for g in gathered]
     if world > 1:
         mx = vals.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
@@ -449,6 +479,15 @@ def run_cuda(args):
                 "identical_to_scan": same}
         if args.workload == "large":
             line["exchange"] = exchange
+        if nvl_all is not None:
+            row_bytes = 4 * (n_ + 1)
+            line["nvlink"] = {
+                "tx_bytes_per_step_by_rank": [r[0] for r in nvl_all],
+                "rx_bytes_per_step_by_rank": [r[1] for r in nvl_all],
+                "source": "NVML NVLINK_THROUGHPUT_DATA_TX/RX summed over links, around the timed steps "
+                          "(includes the end-of-step barriers and, batched, the result gather)",
+                "algorithmic_tx_bytes_per_step_per_rank": (
+                    (world - 1) * row_bytes * (m_ - 1) / world if args.workload == "large" else None)}
         if not args.no_latency and args.workload == "batched":
             line["latency"] = latency_lines(dev)
         if not args.no_cpu_baseline and world == 1 and args.workload == "batched":
