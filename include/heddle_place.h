@@ -129,9 +129,10 @@ typedef struct {
   int64_t kv_caps_stride;
   const int32_t* weights;       /* [B][n] item weights >= 1 or NULL (= 1): an item stands for w  */
                                 /*   trajectories after short-trajectory aggregation; */
-                                /*   group size = sum of weights (R5); sum <= max_n.  Batched    */
-                                /*   (one-CTA-per-problem) kernel only: E_INVALID if n needs the  */
-                                /*   layered kernel                                             */
+                                /*   group size = sum of weights (R5); sum <= max_n (else the    */
+                                /*   problem's E_RANGE).  Scan: the one-CTA-per-problem kernel    */
+                                /*   (E_INVALID if n needs the layered scan); HEDDLE_VALLEY: one  */
+                                /*   CTA per problem or, for large n, the per-layer valley kernel */
   int64_t weights_stride;
   const int32_t* ms;            /* [B] per-problem worker count m_b in [1, m], or NULL (= m for all): a
                                  *   ragged batch, e.g. the simulated-annealing proposals of Alg. 2
@@ -141,6 +142,10 @@ typedef struct {
                                  *   followed by -1 up to index m.  One-CTA-per-problem kernels only
                                  *   (n must fit shared memory; E_INVALID otherwise and in split mode).
                                  *   m_b outside [1, m] gives that problem HEDDLE_E_INVALID.         */
+  const int32_t* ns;            /* [B] per-problem item count n_b in [1, n], or NULL (= n): problem b
+                                 *   uses lengths[b][0..n_b) (weights likewise), e.g. the aggregated
+                                 *   problems of heddle_place_aggregate, whose item counts
+                                 *   differ.  Same kernel restriction and error rule as ms.          */
 } heddle_place_problem;
 
 /* Creates a context on cfg->device: copies and validates the profile (E_RANGE
@@ -246,6 +251,24 @@ int32_t heddle_place_split_plan(int32_t n, int32_t m, int32_t world, int32_t ran
  * weights) and split-mode contexts.  Same per-problem status_out / +inf conventions as solve. */
 heddle_status heddle_place_objective(heddle_place_ctx* ctx, const heddle_place_problem* prob, void* objective_out,
                                      int32_t* status_out, void* stream);
+
+/* ---- short-trajectory aggregation (§5.2) ----
+ * heddle_place_aggregate: for each of B sorted problems (lengths [B][n] of `dtype`, row stride
+ *   lengths_stride, non-increasing as the solve requires), the trajectories with length >=
+ *   threshold stay single items and the shorter ones (a suffix) are cut into consecutive buckets
+ *   of at most `bucket`; a bucket is ONE item: length = its first (largest) member, weight = its
+ *   cardinality (group size = sum of weights, R5).  threshold <= 0: identity.
+ *   Outputs (device): agg_lengths_out [B][n] (dtype) and weights_out [B][n] (rows filled up to
+ *   n_b', padded after), starts_out [B][n+1] (first trajectory of each item, starts[n_b'] = n),
+ *   n_out [B] = n_b'.  Feed them to heddle_place_solve as lengths / weights with ns = n_out.
+ * heddle_place_expand: boundaries of the aggregated solve [B][m+1] -> trajectory boundaries
+ *   (b_j -> starts[b_j], -1 kept).  Both asynchronous on `stream`, no context needed; E_INVALID on
+ *   null pointers, n, B, m or bucket < 1, a negative stride, a NaN threshold or an unknown dtype. */
+heddle_status heddle_place_aggregate(int32_t dtype, const void* lengths, int64_t lengths_stride, int32_t n, int32_t B,
+                                    double threshold, int32_t bucket, void* agg_lengths_out, int32_t* weights_out,
+                                    int32_t* starts_out, int32_t* n_out, void* stream);
+heddle_status heddle_place_expand(const int32_t* agg_boundaries, int32_t m, int32_t B, const int32_t* starts, int32_t n,
+                                  int32_t* boundaries_out, void* stream);
 
 /* ---- device-resident resource manager: Sort-Initialized Simulated Annealing,
  * Alg. 2, P independent chains over sorted MP-degree allocations.  Per

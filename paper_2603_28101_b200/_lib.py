@@ -31,7 +31,7 @@ SYMBOLS = ("heddle_place_init", "heddle_place_solve", "heddle_place_backtrack", 
            "heddle_place_launch_count", "heddle_place_transitions", "heddle_place_destroy",
            "heddle_place_strerror", "heddle_place_nccl_unique_id", "heddle_place_init_split",
            "heddle_place_split_blocks", "heddle_place_split_plan", "heddle_place_debug_violations", "heddle_place_retarget",
-           "heddle_place_objective", "heddle_place_anneal")
+           "heddle_place_objective", "heddle_place_anneal", "heddle_place_aggregate", "heddle_place_expand")
 
 
 class Config(ctypes.Structure):
@@ -49,7 +49,7 @@ class Problem(ctypes.Structure):
                 ("caps", ctypes.c_void_p), ("caps_stride", ctypes.c_int64),
                 ("kv_caps", ctypes.c_void_p), ("kv_caps_stride", ctypes.c_int64),
                 ("weights", ctypes.c_void_p), ("weights_stride", ctypes.c_int64),
-                ("ms", ctypes.c_void_p)]
+                ("ms", ctypes.c_void_p), ("ns", ctypes.c_void_p)]
 
 
 class AnnealArgs(ctypes.Structure):
@@ -91,6 +91,11 @@ def lib() -> ctypes.CDLL:
         L.heddle_place_query.argtypes = [vp, ctypes.c_int32, vp, vp, vp, vp, vp, vp]
         L.heddle_place_anneal.argtypes = [vp, ctypes.POINTER(AnnealArgs), ctypes.POINTER(AnnealOut), vp]
         L.heddle_place_anneal.restype = ctypes.c_int
+        L.heddle_place_aggregate.argtypes = [ctypes.c_int32, vp, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                             ctypes.c_double, ctypes.c_int32, vp, vp, vp, vp, vp]
+        L.heddle_place_aggregate.restype = ctypes.c_int
+        L.heddle_place_expand.argtypes = [vp, ctypes.c_int32, ctypes.c_int32, vp, ctypes.c_int32, vp, vp]
+        L.heddle_place_expand.restype = ctypes.c_int
         L.heddle_place_query.restype = ctypes.c_int
         L.heddle_place_solve_host.argtypes = [vp, ctypes.POINTER(Problem), vp, vp, vp, vp,
                                               ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]

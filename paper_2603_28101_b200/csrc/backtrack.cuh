@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(32 * kK4Warps) k4_backtrack(SolveArgs a, int32
   const int lane = threadIdx.x & 31;
   const int b = blockIdx.x * kK4Warps + (threadIdx.x >> 5);
   if (b >= a.B) return;
-  const int n = a.n, M = a.m, m = prob_m(a, b);   // M: row stride; m: this problem's workers
+  const int N = a.n, M = a.m, n = prob_n(a, b), m = prob_m(a, b);   // N, M: strides; n, m: this problem's
   int32_t* out = bounds + (int64_t)b * (M + 1);
   if (a.status[b] != HEDDLE_OK) {
     for (int j = lane; j <= M; j += 32) out[j] = -1;
@@ -102,10 +102,10 @@ __global__ void __launch_bounds__(32 * kK4Warps) k4_backtrack(SolveArgs a, int32
   }
   for (int j = m + 1 + lane; j <= M; j += 32) out[j] = -1;   // ragged batch: unused tail
   const L* gL = reinterpret_cast<const L*>(a.lengths) + (int64_t)b * a.ls;
-  const D* gdp = reinterpret_cast<const D*>(a.dpws) + (int64_t)b * (M + 1) * (n + 1);
+  const D* gdp = reinterpret_cast<const D*>(a.dpws) + (int64_t)b * (M + 1) * (N + 1);
   const G* gtab = reinterpret_cast<const G*>(a.gtab);
-  const S* gSp = KV ? reinterpret_cast<const S*>(a.spws) + (int64_t)b * (n + 1) : nullptr;
-  const int32_t* gWp = W ? a.wpws + (int64_t)b * (n + 1) : nullptr;
+  const S* gSp = KV ? reinterpret_cast<const S*>(a.spws) + (int64_t)b * (N + 1) : nullptr;
+  const int32_t* gWp = W ? a.wpws + (int64_t)b * (N + 1) : nullptr;
   int cur = n;
   if (lane == 0) out[m] = n;
   for (int j = m; j >= 2; --j) {
@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(kK4CtaThreads) k4_backtrack_cta(SolveArgs a, i
   using S = typename SpT<DT>::type;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int b = blockIdx.x;
-  const int n = a.n, M = a.m, m = prob_m(a, b);
+  const int N = a.n, M = a.m, n = prob_n(a, b), m = prob_m(a, b);
   int32_t* out = bounds + (int64_t)b * (M + 1);
   if (a.status[b] != HEDDLE_OK) {
     for (int j = tid; j <= M; j += kK4CtaThreads) out[j] = -1;
@@ -157,10 +157,10 @@ __global__ void __launch_bounds__(kK4CtaThreads) k4_backtrack_cta(SolveArgs a, i
   for (int j = m + 1 + tid; j <= M; j += kK4CtaThreads) out[j] = -1;
   __shared__ int s_lo, s_found, s_row;
   const L* gL = reinterpret_cast<const L*>(a.lengths) + (int64_t)b * a.ls;
-  const D* gdp = reinterpret_cast<const D*>(a.dpws) + (int64_t)b * (M + 1) * (n + 1);
+  const D* gdp = reinterpret_cast<const D*>(a.dpws) + (int64_t)b * (M + 1) * (N + 1);
   const G* gtab = reinterpret_cast<const G*>(a.gtab);
-  const S* gSp = KV ? reinterpret_cast<const S*>(a.spws) + (int64_t)b * (n + 1) : nullptr;
-  const int32_t* gWp = W ? a.wpws + (int64_t)b * (n + 1) : nullptr;
+  const S* gSp = KV ? reinterpret_cast<const S*>(a.spws) + (int64_t)b * (N + 1) : nullptr;
+  const int32_t* gWp = W ? a.wpws + (int64_t)b * (N + 1) : nullptr;
   int cur = n;
   if (tid == 0) out[m] = n;
   for (int j = m; j >= 2; --j) {
@@ -223,15 +223,16 @@ __global__ void __launch_bounds__(32 * kK4Warps) k4_query(SolveArgs a, int nq, c
   const int lane = threadIdx.x & 31;
   const int q = blockIdx.x * kK4Warps + (threadIdx.x >> 5);
   if (q >= nq) return;
-  const int n = a.n, M = a.m;
+  const int N = a.n, M = a.m;
   const int b = qb[q], j = qj[q], cur = qi[q];
   const int m = (b >= 0 && b < a.B) ? prob_m(a, b) : 0;
+  const int n = (b >= 0 && b < a.B) ? prob_n(a, b) : 0;
   D val = T::inf();
   int found = -1;
   const bool ok = b >= 0 && b < a.B && j >= 1 && j <= m && cur >= j && cur <= n - m + j &&
                   (j < m || cur == n || m == 1) && a.status[b] == HEDDLE_OK;
   if (ok) {
-    const D* gdp = reinterpret_cast<const D*>(a.dpws) + (int64_t)b * (M + 1) * (n + 1);
+    const D* gdp = reinterpret_cast<const D*>(a.dpws) + (int64_t)b * (M + 1) * (N + 1);
     val = T::norm(gdp[(int64_t)j * (n + 1) + cur]);
     if (val != T::inf()) {
       if (j == 1) {
@@ -239,8 +240,8 @@ __global__ void __launch_bounds__(32 * kK4Warps) k4_query(SolveArgs a, int nq, c
       } else {
         const L* gL = reinterpret_cast<const L*>(a.lengths) + (int64_t)b * a.ls;
         const G* gtab = reinterpret_cast<const G*>(a.gtab);
-        const S* gSp = KV ? reinterpret_cast<const S*>(a.spws) + (int64_t)b * (n + 1) : nullptr;
-        const int32_t* gWp = W ? a.wpws + (int64_t)b * (n + 1) : nullptr;
+        const S* gSp = KV ? reinterpret_cast<const S*>(a.spws) + (int64_t)b * (N + 1) : nullptr;
+        const int32_t* gWp = W ? a.wpws + (int64_t)b * (N + 1) : nullptr;
         const int d = a.degrees[(int64_t)b * a.ds + j - 1];
         int row = 0;
         for (int r = 0; r < a.D; ++r) row = (a.prof_deg[r] == d) ? r : row;

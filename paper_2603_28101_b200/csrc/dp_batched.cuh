@@ -80,11 +80,16 @@ struct SolveArgs {
   int vscan;               // valley kernel: descent prefixes shorter than this are scanned (K8)
   int2* rowcap;            // [B][m] {profile row, cap} per worker, written by the K3/K5 prologue, or null
   const int32_t* ms;       // [B] per-problem worker count (ragged m, <= m) or null (= m); one-CTA kernels
+  const int32_t* ns;       // [B] per-problem item count (ragged n, <= n) or null (= n); one-CTA kernels
 };
 
 // worker count of problem b (ragged batches: SA proposals of different sizes in one launch);
 // m stays the row stride of degrees / caps / boundaries and of the dp workspace
 __device__ __forceinline__ int prob_m(const SolveArgs& a, int b) { return a.ms ? __ldg(a.ms + b) : a.m; }
+// item count of problem b (ragged batches: e.g. aggregated problems).  n stays the
+// stride of lengths / weights rows and of the per-problem workspace slabs; inside its slab a
+// problem's dp rows are packed with its own stride n_b + 1 (every kernel addresses them alike)
+__device__ __forceinline__ int prob_n(const SolveArgs& a, int b) { return a.ns ? __ldg(a.ns + b) : a.n; }
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
@@ -326,14 +331,25 @@ __device__ __forceinline__ void sweep_weighted(const typename Tr<DT, SR>::L* __r
 // weight prefix sums (also written to the workspace for the backtrack).  Returns the problem's
 // status; a non-zero status is already recorded (status, objective) and the CTA must return.
 template <int DT, int SR, bool KV, bool W, int NT>
-__device__ __forceinline__ int load_problem(const SolveArgs& a, int b, int m, typename Tr<DT, SR>::L* sL, int* srow,
-                                            int* scap, int64_t* skv, typename SpT<DT>::type* sSp, int* sWp,
-                                            int& s_err) {
+__device__ __forceinline__ int load_problem(const SolveArgs& a, int b, int n, int m, typename Tr<DT, SR>::L* sL,
+                                            int* srow, int* scap, int64_t* skv, typename SpT<DT>::type* sSp,
+                                            int* sWp, int& s_err) {
   using T = Tr<DT, SR>;
   using L = typename T::L;
   using D = typename T::D;
   using S = typename SpT<DT>::type;
-  const int n = a.n, tid = threadIdx.x;   // m: this problem's worker count (prob_m)
+  const int tid = threadIdx.x;   // n, m: this problem's item and worker counts (prob_n, prob_m)
+  if (n < 1 || n > a.n) {        // ragged item count outside [1, n]
+    if (tid == 0) {
+      a.status[b] = HEDDLE_E_INVALID;
+      if (a.status_out) a.status_out[b] = HEDDLE_E_INVALID;
+      if constexpr (DT == HEDDLE_U32 && SR == HEDDLE_MINPLUS)
+        reinterpret_cast<uint64_t*>(a.objective)[b] = ~0ull;
+      else
+        reinterpret_cast<D*>(a.objective)[b] = T::inf();
+    }
+    return HEDDLE_E_INVALID;
+  }
   const L* gL = reinterpret_cast<const L*>(a.lengths) + (int64_t)b * a.ls;
   // ---------------- load + validate (lengths sorted/finite/positive, degrees known and sorted)
   if (tid == 0) {
@@ -404,11 +420,11 @@ __device__ __forceinline__ int load_problem(const SolveArgs& a, int b, int m, ty
       for (int t = 0; t < n; ++t) { acc += (S)sL[t]; sSp[t + 1] = acc; }
     }
     __syncthreads();
-    S* gSp = reinterpret_cast<S*>(a.spws) + (int64_t)b * (n + 1);   // for the backtrack
+    S* gSp = reinterpret_cast<S*>(a.spws) + (int64_t)b * (a.n + 1);   // for the backtrack
     for (int t = tid; t <= n; t += NT) gSp[t] = sSp[t];
   }
   if constexpr (W) {
-    int32_t* gWp = a.wpws + (int64_t)b * (n + 1);   // for the backtrack
+    int32_t* gWp = a.wpws + (int64_t)b * (a.n + 1);   // for the backtrack
     for (int t = tid; t <= n; t += NT) gWp[t] = sWp[t];
   }
   return 0;
@@ -430,10 +446,10 @@ __global__ void __launch_bounds__(kK2Threads, (SR == HEDDLE_MINMAX && DT != HEDD
   using D = typename T::D;
   using S = typename SpT<DT>::type;
   extern __shared__ __align__(16) unsigned char smem[];
-  const int n = a.n, M = a.m, b = blockIdx.x;   // M: row stride (max workers); m: this problem's
-  const int m = prob_m(a, b);
+  const int N = a.n, M = a.m, b = blockIdx.x;   // N, M: strides (max items / workers)
+  const int n = prob_n(a, b), m = prob_m(a, b);  // this problem's
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const K2Smem<DT, SR> lay(n, M, KV, W);
+  const K2Smem<DT, SR> lay(N, M, KV, W);
   G* sG = reinterpret_cast<G*>(smem + lay.gOff);
   G* sG2 = reinterpret_cast<G*>(smem + lay.g2Off);
   L* sL = reinterpret_cast<L*>(smem + lay.lOff);
@@ -449,11 +465,11 @@ __global__ void __launch_bounds__(kK2Threads, (SR == HEDDLE_MINMAX && DT != HEDD
   __shared__ D s_redv[kK2Warps];
   __shared__ int s_redk[kK2Warps];
 
-  D* gdp = reinterpret_cast<D*>(a.dpws) + (int64_t)b * (M + 1) * (n + 1);
-  int32_t* gpar = KP ? a.parws + (int64_t)b * (M + 1) * (n + 1) : nullptr;
+  D* gdp = reinterpret_cast<D*>(a.dpws) + (int64_t)b * (M + 1) * (N + 1);
+  int32_t* gpar = KP ? a.parws + (int64_t)b * (M + 1) * (N + 1) : nullptr;
   const G* gtab = reinterpret_cast<const G*>(a.gtab);
 
-  if (load_problem<DT, SR, KV, W, kK2Threads>(a, b, m, sL, srow, scap, skv, sSp, sWp, s_err) != 0) return;
+  if (load_problem<DT, SR, KV, W, kK2Threads>(a, b, n, m, sL, srow, scap, skv, sSp, sWp, s_err) != 0) return;
   for (int t = tid; t < align4(n + kLPad); t += kK2Threads) { sdp0[t] = T::inf(); sdp1[t] = T::inf(); }
 
   // ---------------- layers

@@ -15,6 +15,7 @@
 #include <vector>
 #include <algorithm>
 
+#include "aggregate.cuh"
 #include "anneal.cuh"
 #include "backtrack.cuh"
 #include "dp_batched.cuh"
@@ -246,8 +247,8 @@ bool use_layered(const heddle_place_ctx* x, int n, int m, int B) {
 // those kernels can take pipelined host inputs, see heddle_place_solve_host.)
 bool per_problem_kernel(const heddle_place_ctx* x, int n, int m, int B, bool kv, bool wt) {
   if (x->split_world > 1) return false;
-  if (x->flags & HEDDLE_VALLEY)   // K8 whenever the problem fits shared memory (weights: must fit)
-    return wt || (!(x->flags & HEDDLE_FORCE_LAYERED) && k8_smem(x->dtype, n, m, kv, false) <= x->k8_smem_max);
+  if (x->flags & HEDDLE_VALLEY)   // K8 whenever the problem fits shared memory, else K8L
+    return !(x->flags & HEDDLE_FORCE_LAYERED) && k8_smem(x->dtype, n, m, kv, wt) <= x->k8_smem_max;
   if (wt || (x->flags & HEDDLE_FORCE_BATCHED)) return true;   // weights: batched kernel only
   if (x->flags & HEDDLE_FORCE_LAYERED) return false;
   return k2_smem(x->dtype, x->semiring, n, m, kv, wt) <= x->k2_smem_max && !use_layered(x, n, m, B);
@@ -850,7 +851,6 @@ heddle_status heddle_place_init(const heddle_place_config* c, heddle_place_ctx**
 heddle_status solve_valley_layered(heddle_place_ctx* x, SolveArgs& a, bool kp, bool kv, cudaStream_t s) {
   const int dt = x->dtype, sr = x->semiring;
   const int n = a.n, m = a.m, B = a.B;
-  if (a.w) return HEDDLE_E_INVALID;   // aggregation weights: one-CTA-per-problem kernel only
   if (kp) {   // parents off the computed region read -1
     const int64_t cells = (int64_t)B * (m + 1) * (n + 1);
     const int fill_grid = (int)std::min<int64_t>((cells + 255) / 256, (int64_t)x->num_sms * 16);
@@ -875,7 +875,11 @@ heddle_status solve_valley_layered(heddle_place_ctx* x, SolveArgs& a, bool kp, b
   }
   pro_for(dt, sr, kp, kv)<<<B, 256, 0, s>>>(a);
   x->launches++;
-  K8LFn fn = k8l_for(dt, kp, kv);
+  if (a.w) {   // aggregation weights (R5): prefix sums for the group sizes
+    k8l_weights<<<(B + 127) / 128, 128, 0, s>>>(a);
+    x->launches++;
+  }
+  K8LFn fn = k8l_for(dt, kp, kv, a.w != nullptr);
   for (int j = 1; j <= m; ++j) {
     const int ilo = (j == 1) ? 1 : (j == m ? n : j), ihi = (j == 1 || j < m) ? n - m + j : n;
     const int warps = ((ihi >> 5) - (ilo >> 5) + 1 + 3) / 4;
@@ -916,7 +920,7 @@ static heddle_status solve_impl(heddle_place_ctx* x, const heddle_place_problem*
   const int smem2 = valley ? k8_smem(x->dtype, p->n, p->m, kv, wt) : k2_smem(x->dtype, x->semiring, p->n, p->m, kv, wt);
   const bool fits = smem2 <= (valley ? x->k8_smem_max : x->k2_smem_max);
   const bool wide = (x->dtype == HEDDLE_F64) || (x->dtype == HEDDLE_U32 && x->semiring == HEDDLE_MINPLUS);
-  const bool ragged = p->ms != nullptr;   // per-problem worker counts: one-CTA-per-problem kernels only
+  const bool ragged = p->ms != nullptr || p->ns != nullptr;   // per-problem sizes: one-CTA-per-problem kernels only
   const bool layered = !ragged && !per_problem_kernel(x, p->n, p->m, p->B, kv, wt);
   if (!layered && !fits) return HEDDLE_E_INVALID;   // n too large for the one-CTA-per-problem kernel
   if (layered && kp && wide && !valley) return HEDDLE_E_INVALID;   // packed (value, split) atomics: 32-bit values
@@ -937,6 +941,7 @@ static heddle_status solve_impl(heddle_place_ctx* x, const heddle_place_problem*
   a.w = p->weights;
   a.ws = p->weights_stride;
   a.ms = p->ms;
+  a.ns = p->ns;
   if (wt && !x->d_wp) {
     if (cudaMalloc(&x->d_wp, 4 * (size_t)x->max_batch * (x->max_n + 1)) != cudaSuccess) { cudaGetLastError(); return HEDDLE_E_NOMEM; }
   }
@@ -989,6 +994,7 @@ heddle_status heddle_place_backtrack(heddle_place_ctx* x, int32_t* boundaries_ou
   if (!x || !boundaries_out) return HEDDLE_E_INVALID;
   if (!x->solved) return HEDDLE_E_STATE;
   if (parents_out && !(x->flags & HEDDLE_KEEP_PARENTS)) return HEDDLE_E_STATE;
+  if (parents_out && x->last.ns) return HEDDLE_E_INVALID;   // ragged n: rows are packed per problem
   DeviceGuard guard(x->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const SolveArgs& a = x->last;
@@ -1045,9 +1051,9 @@ heddle_status heddle_place_solve_host(heddle_place_ctx* x, const heddle_place_pr
   const int64_t wrows = p.weights ? (p.weights_stride == 0 ? 1 : B) : 0;
   auto al = [](size_t v) { return (v + 255) & ~(size_t)255; };
   const size_t bl = al(es * lrows * n), bd = al(4 * drows * m), bc = al(4 * crows * m), bk = al(8 * krows * m);
-  const size_t bw = al(4 * wrows * n), bm = p.ms ? al(4 * B) : 0;
+  const size_t bw = al(4 * wrows * n), bm = p.ms ? al(4 * B) : 0, bn = p.ns ? al(4 * B) : 0;
   const size_t bo = al(8 * B), bb = al(4 * B * (m + 1)), bs = al(4 * B);
-  const size_t need = bl + bd + bc + bk + bo + bb + bs + bw + bm;
+  const size_t need = bl + bd + bc + bk + bo + bb + bs + bw + bm + bn;
   if (need > x->stage_bytes) {
     cudaFree(x->d_stage);
     x->d_stage = nullptr;
@@ -1059,6 +1065,7 @@ heddle_status heddle_place_solve_host(heddle_place_ctx* x, const heddle_place_pr
   char *dl = base, *dd = dl + bl, *dc = dd + bd, *dk = dc + bc, *dob = dk + bk, *dbd = dob + bo, *dst = dbd + bb;
   char* dw = dst + bs;
   char* dms = dw + bw;
+  char* dns = dms + bm;
   int64_t h2d = 0, d2h = 0;
   // Pipelined inputs (batched kernel, many problems): the host->device copies run on a copy stream
   // in chunks of problems, each chunk followed by a 4-byte copy of the call's epoch into its ready
@@ -1066,7 +1073,7 @@ heddle_status heddle_place_solve_host(heddle_place_ctx* x, const heddle_place_pr
   // acquire poll) for its problem's chunk, so only the first chunk's copy is exposed.  Copies run on
   // the copy engines, never on the SMs the waiting CTAs hold, so the wait always ends.
   const bool kv = p.kv_caps != nullptr, wt = p.weights != nullptr;
-  const bool batched_path = p.ms != nullptr || per_problem_kernel(x, p.n, p.m, p.B, kv, wt);
+  const bool batched_path = p.ms != nullptr || p.ns != nullptr || per_problem_kernel(x, p.n, p.m, p.B, kv, wt);
   int64_t chunk = std::max<int64_t>(kPipeMinChunk, (B + kPipeChunks - 1) / kPipeChunks);
   if (const char* e = std::getenv("HEDDLE_PLACE_HOST_CHUNK")) chunk = std::max(1, std::atoi(e));   // tuning
   const int64_t chunks = batched_path ? (B + chunk - 1) / chunk : 1;
@@ -1113,7 +1120,8 @@ heddle_status heddle_place_solve_host(heddle_place_ctx* x, const heddle_place_pr
         !up(dc, p.caps, crows, m, p.caps_stride, 4, b0, b1) ||
         !up(dk, p.kv_caps, krows, m, p.kv_caps_stride, 8, b0, b1) ||
         !up(dw, p.weights, wrows, n, p.weights_stride, 4, b0, b1) ||
-        !up(dms, p.ms, p.ms ? B : 0, 1, 1, 4, b0, b1))
+        !up(dms, p.ms, p.ms ? B : 0, 1, 1, 4, b0, b1) ||
+        !up(dns, p.ns, p.ns ? B : 0, 1, 1, 4, b0, b1))
       return HEDDLE_E_CUDA;
     if (pipe && cudaMemcpyAsync(x->d_chunk_ready + c, x->h_epoch, 4, cudaMemcpyHostToDevice, cs) != cudaSuccess)
       return HEDDLE_E_CUDA;
@@ -1131,6 +1139,7 @@ heddle_status heddle_place_solve_host(heddle_place_ctx* x, const heddle_place_pr
   q.weights = p.weights ? reinterpret_cast<const int32_t*>(dw) : nullptr;
   q.weights_stride = p.weights_stride == 0 ? 0 : n;
   q.ms = p.ms ? reinterpret_cast<const int32_t*>(dms) : nullptr;
+  q.ns = p.ns ? reinterpret_cast<const int32_t*>(dns) : nullptr;
   heddle_status st =
       solve_impl(x, &q, dob, reinterpret_cast<int32_t*>(dst), stream, pipe ? x->d_chunk_ready : nullptr, epoch, (int)chunk);
   if (st != HEDDLE_OK) {
@@ -1360,6 +1369,7 @@ heddle_status heddle_place_objective(heddle_place_ctx* x, const heddle_place_pro
   a.kv = p->kv_caps;
   a.kvs = p->kv_caps_stride;
   a.ms = p->ms;
+  a.ns = p->ns;
   a.gtab = x->d_gtab;
   a.gstride = x->gstride;
   a.prof_deg = x->d_prof_deg;
@@ -1390,6 +1400,37 @@ heddle_status heddle_place_objective(heddle_place_ctx* x, const heddle_place_pro
 #undef HP_K7
   x->launches++;
   x->solved = false;   // no dp rows: a following backtrack is a state error
+  return cudaGetLastError() == cudaSuccess ? HEDDLE_OK : HEDDLE_E_CUDA;
+}
+
+heddle_status heddle_place_aggregate(int32_t dtype, const void* lengths, int64_t lengths_stride, int32_t n, int32_t B,
+                                    double threshold, int32_t bucket, void* agg_lengths_out, int32_t* weights_out,
+                                    int32_t* starts_out, int32_t* n_out, void* stream) {
+  if (!lengths || !agg_lengths_out || !weights_out || !starts_out || !n_out || n < 1 || B < 1 || bucket < 1 ||
+      lengths_stride < 0 || std::isnan(threshold))
+    return HEDDLE_E_INVALID;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (dtype == HEDDLE_F32)
+    k10_aggregate<float><<<B, 128, 0, s>>>(static_cast<const float*>(lengths), lengths_stride, n, threshold, bucket,
+                                           static_cast<float*>(agg_lengths_out), weights_out, starts_out, n_out);
+  else if (dtype == HEDDLE_F64)
+    k10_aggregate<double><<<B, 128, 0, s>>>(static_cast<const double*>(lengths), lengths_stride, n, threshold, bucket,
+                                            static_cast<double*>(agg_lengths_out), weights_out, starts_out, n_out);
+  else if (dtype == HEDDLE_U32)
+    k10_aggregate<uint32_t><<<B, 128, 0, s>>>(static_cast<const uint32_t*>(lengths), lengths_stride, n, threshold,
+                                              bucket, static_cast<uint32_t*>(agg_lengths_out), weights_out,
+                                              starts_out, n_out);
+  else
+    return HEDDLE_E_INVALID;
+  return cudaGetLastError() == cudaSuccess ? HEDDLE_OK : HEDDLE_E_CUDA;
+}
+
+heddle_status heddle_place_expand(const int32_t* agg_boundaries, int32_t m, int32_t B, const int32_t* starts, int32_t n,
+                                  int32_t* boundaries_out, void* stream) {
+  if (!agg_boundaries || !starts || !boundaries_out || m < 1 || B < 1 || n < 1) return HEDDLE_E_INVALID;
+  const int64_t total = (int64_t)B * (m + 1);
+  k10_expand<<<(unsigned)((total + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(agg_boundaries, m, B,
+                                                                                             starts, n, boundaries_out);
   return cudaGetLastError() == cudaSuccess ? HEDDLE_OK : HEDDLE_E_CUDA;
 }
 

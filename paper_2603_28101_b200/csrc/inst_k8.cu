@@ -25,14 +25,18 @@ K8Fn k8_for(int dt, bool kp, bool kv, bool w, bool wide) {
   return pick_k8<HEDDLE_U32>(kp, kv, w, wide);
 }
 template <int DT>
-K8LFn pick_k8l(bool kp, bool kv) {
+K8LFn pick_k8l(bool kp, bool kv, bool w) {
+  if (w) {
+    if (kp) return kv ? k8l_layer<DT, true, true, true> : k8l_layer<DT, true, false, true>;
+    return kv ? k8l_layer<DT, false, true, true> : k8l_layer<DT, false, false, true>;
+  }
   if (kp) return kv ? k8l_layer<DT, true, true> : k8l_layer<DT, true, false>;
   return kv ? k8l_layer<DT, false, true> : k8l_layer<DT, false, false>;
 }
-K8LFn k8l_for(int dt, bool kp, bool kv) {
-  if (dt == HEDDLE_F32) return pick_k8l<HEDDLE_F32>(kp, kv);
-  if (dt == HEDDLE_F64) return pick_k8l<HEDDLE_F64>(kp, kv);
-  return pick_k8l<HEDDLE_U32>(kp, kv);
+K8LFn k8l_for(int dt, bool kp, bool kv, bool w) {
+  if (dt == HEDDLE_F32) return pick_k8l<HEDDLE_F32>(kp, kv, w);
+  if (dt == HEDDLE_F64) return pick_k8l<HEDDLE_F64>(kp, kv, w);
+  return pick_k8l<HEDDLE_U32>(kp, kv, w);
 }
 K8SFn k8lr_for(int dt) {
   if (dt == HEDDLE_F32) return k8l_rowprep<HEDDLE_F32>;

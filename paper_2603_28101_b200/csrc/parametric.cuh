@@ -105,8 +105,8 @@ __global__ void __launch_bounds__(WPP == 1 ? 32 * kK7Warps : 32 * WPP) k7_parame
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int b = WPP == 1 ? (int)(blockIdx.x * kK7Warps + warp) : (int)blockIdx.x;
   if (b >= a.B) return;
-  const int n = a.n, m0 = prob_m(a, b);   // ragged batches: this problem's worker count
-  const int m = min(max(m0, 1), a.m);
+  const int m0 = prob_m(a, b), n0 = prob_n(a, b);   // ragged batches: this problem's counts
+  const int m = min(max(m0, 1), a.m), n = min(max(n0, 1), a.n);
   const L* gL = reinterpret_cast<const L*>(a.lengths) + (int64_t)b * a.ls;
   __shared__ int s_err;
   __shared__ unsigned s_feas[WPP == 1 ? 1 : WPP];
@@ -131,10 +131,10 @@ __global__ void __launch_bounds__(WPP == 1 ? 32 * kK7Warps : 32 * WPP) k7_parame
     }
     err = __reduce_min_sync(0xffffffffu, err ? err : INT_MAX);
     err = err == INT_MAX ? 0 : err;
-    if (m0 != m) err = HEDDLE_E_INVALID;
+    if (m0 != m || n0 != n) err = HEDDLE_E_INVALID;
     if (err == 0 && n < m) err = HEDDLE_E_INFEASIBLE;
   }
-  S* gSp = KV ? reinterpret_cast<S*>(a.spws) + (int64_t)b * (n + 1) : nullptr;
+  S* gSp = KV ? reinterpret_cast<S*>(a.spws) + (int64_t)b * (a.n + 1) : nullptr;
   if ((WPP == 1 || warp == 0) && err == 0 && KV) {   // token prefix sums, left to right (R6)
     if (lane == 0) {
       S acc = 0;

@@ -242,9 +242,9 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k8_valley(SolveArgs a) {
   using D = typename T::D;
   using S = typename SpT<DT>::type;
   extern __shared__ __align__(16) unsigned char smem[];
-  const int n = a.n, M = a.m, b = blockIdx.x, tid = threadIdx.x;   // M: row stride; m: this problem's
-  const int m = prob_m(a, b);
-  const K8Smem<DT> lay(n, M, KV, W);
+  const int N = a.n, M = a.m, b = blockIdx.x, tid = threadIdx.x;   // N, M: strides; n, m: this problem's
+  const int n = prob_n(a, b), m = prob_m(a, b);
+  const K8Smem<DT> lay(N, M, KV, W);
   L* sL = reinterpret_cast<L*>(smem + lay.lOff);
   G* sG = W ? nullptr : reinterpret_cast<G*>(smem + lay.gOff);
   D* const sdp0 = reinterpret_cast<D*>(smem + lay.d0Off);
@@ -259,10 +259,10 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k8_valley(SolveArgs a) {
   int64_t* skv = reinterpret_cast<int64_t*>(smem + lay.kvOff);
   __shared__ int s_err, s_dlast[2];
   if (tid == 0) { s_dlast[0] = -1; s_dlast[1] = -1; }
-  if (load_problem<DT, HEDDLE_MINMAX, KV, W, NT>(a, b, m, sL, srow, scap, skv, sSp, sWp, s_err) != 0) return;
+  if (load_problem<DT, HEDDLE_MINMAX, KV, W, NT>(a, b, n, m, sL, srow, scap, skv, sSp, sWp, s_err) != 0) return;
   __syncthreads();
-  D* gdp = reinterpret_cast<D*>(a.dpws) + (int64_t)b * (M + 1) * (n + 1);
-  int32_t* gpar = KP ? a.parws + (int64_t)b * (M + 1) * (n + 1) : nullptr;
+  D* gdp = reinterpret_cast<D*>(a.dpws) + (int64_t)b * (M + 1) * (N + 1);
+  int32_t* gpar = KP ? a.parws + (int64_t)b * (M + 1) * (N + 1) : nullptr;
   const G* gtab = reinterpret_cast<const G*>(a.gtab);
   const int nb = vblocks(n);
 
@@ -396,7 +396,7 @@ struct ValleyWs {                // K8L range-minimum workspace (per problem, ro
   int nbmax, lvmax;
 };
 
-template <int DT, bool KP, bool KV>
+template <int DT, bool KP, bool KV, bool W = false>
 __global__ void __launch_bounds__(32 * kK8LWarps, 4) k8l_layer(SolveArgs a, int j, ValleyWs w) {
   using T = Tr<DT, HEDDLE_MINMAX>;
   using L = typename T::L;
@@ -422,9 +422,10 @@ __global__ void __launch_bounds__(32 * kK8LWarps, 4) k8l_layer(SolveArgs a, int 
                      reinterpret_cast<const D*>(w.bm) + ((int64_t)pp * a.B + b) * nb,
                      reinterpret_cast<const D*>(w.sp) + (int64_t)b * (w.lvmax - 1) * nb, nb,
                      j > 1 ? w.dlast[b] : -1};
-  Valley<DT, KV, false> V{reinterpret_cast<const L*>(a.lengths) + (int64_t)b * a.ls, rm,
-                          reinterpret_cast<const G*>(a.gtab) + (int64_t)row * a.gstride,
-                          KV ? reinterpret_cast<const S*>(a.spws) + (int64_t)b * (n + 1) : nullptr, nullptr,
+  Valley<DT, KV, W> V{reinterpret_cast<const L*>(a.lengths) + (int64_t)b * a.ls, rm,
+                      reinterpret_cast<const G*>(a.gtab) + (int64_t)row * a.gstride,
+                      KV ? reinterpret_cast<const S*>(a.spws) + (int64_t)b * (n + 1) : nullptr,
+                      W ? a.wpws + (int64_t)b * (n + 1) : nullptr,
                           (cap >= 0 && cap < a.gstride - 1) ? cap : a.gstride - 1,
                           KV ? a.kv[(int64_t)b * a.kvs + j - 1] : -1, false};
   const int x0 = (blk0 << 5) + kK8LRun * lane;
@@ -457,6 +458,30 @@ __global__ void __launch_bounds__(32 * kK8LWarps, 4) k8l_layer(SolveArgs a, int 
     block_masks<T>(s_row[warp] + 32 * lane, ilo - (blk << 5), ihi - (blk << 5), mk + (blk << 5), bmj + blk);
   }
 }
+
+#ifndef HEDDLE_INST_TU   // non-template kernels: defined in heddle_place.cu's translation unit only
+// Weight prefix sums Wp[b][0..n] of aggregated items (R5) for the layered valley solve, after the
+// layered prologue: exact, left to right, one thread per problem; a weight < 1 or a total beyond
+// the cost table makes the problem's status HEDDLE_E_RANGE (as in the one-CTA kernels).
+__global__ void k8l_weights(SolveArgs a) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= a.B || a.status[b] != HEDDLE_OK) return;
+  int32_t* wp = a.wpws + (int64_t)b * (a.n + 1);
+  int acc = 0;
+  bool ok = true;
+  wp[0] = 0;
+  for (int t = 0; t < a.n; ++t) {
+    const int wt = a.w[(int64_t)b * a.ws + t];
+    ok = ok && wt >= 1 && acc <= a.gstride - 1 - wt;
+    acc += wt > 0 ? wt : 0;
+    wp[t + 1] = acc;
+  }
+  if (!ok) {
+    a.status[b] = HEDDLE_E_RANGE;
+    if (a.status_out) a.status_out[b] = HEDDLE_E_RANGE;
+  }
+}
+#endif
 
 // Row j's range-minimum extras, after k8l_layer(j) (one CTA per problem): its last descent, the
 // suffix minima of the descent prefix, and sparse levels >= 1 over the prefix's block minima.

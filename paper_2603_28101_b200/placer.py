@@ -104,7 +104,7 @@ class Placer:
     def launches(self) -> int:
         return int(C.lib().heddle_place_launch_count(self._h))
 
-    def _problem(self, lengths, degrees, caps, kv_caps, weights=None, ms=None):
+    def _problem(self, lengths, degrees, caps, kv_caps, weights=None, ms=None, ns=None):
         if lengths.dim() == 1:
             lengths = lengths[None, :]
         B, n = lengths.shape
@@ -123,25 +123,29 @@ class Placer:
         Cp, cs = _rows(None if caps is None else caps.to(torch.int32), B, m, "caps")
         K, ks = _rows(None if kv_caps is None else kv_caps.to(torch.int64), B, m, "kv_caps")
         Wt, wts = _rows(None if weights is None else weights.to(torch.int32), B, n, "weights")
-        Ms = None
-        if ms is not None:
-            if ms.device != self.device:
-                raise ValueError(f"ms must live on {self.device}")
-            Ms = ms.to(torch.int32).contiguous()
-            if Ms.shape != (B,):
-                raise ValueError(f"ms: expected [{B}], got {tuple(Ms.shape)}")
-        keep = (L, D, Cp, K, Wt, Ms)
+        def counts(t, nm):
+            if t is None:
+                return None
+            if t.device != self.device:
+                raise ValueError(f"{nm} must live on {self.device}")
+            t = t.to(torch.int32).contiguous()
+            if t.shape != (B,):
+                raise ValueError(f"{nm}: expected [{B}], got {tuple(t.shape)}")
+            return t
+        Ms, Ns = counts(ms, "ms"), counts(ns, "ns")
+        keep = (L, D, Cp, K, Wt, Ms, Ns)
         p = C.Problem(n, m, B, L.data_ptr(), ls, D.data_ptr(), ds, Cp.data_ptr() if Cp is not None else None, cs,
                       K.data_ptr() if K is not None else None, ks, Wt.data_ptr() if Wt is not None else None, wts,
-                      Ms.data_ptr() if Ms is not None else None)
+                      Ms.data_ptr() if Ms is not None else None, Ns.data_ptr() if Ns is not None else None)
         return p, keep, B, n, m
 
-    def solve(self, lengths, degrees, caps=None, kv_caps=None, stream=None, weights=None, ms=None):
+    def solve(self, lengths, degrees, caps=None, kv_caps=None, stream=None, weights=None, ms=None, ns=None):
         """Enqueue the DP on `stream` (default: torch's current stream).  Returns
         (objective[B], status[B]) device tensors.  `weights` ([B, n] int >= 1): aggregated items
         (short-trajectory aggregation); group size = sum of weights.  `ms` ([B] int):
-        per-problem worker counts of a ragged batch (degrees padded to [B, max m])."""
-        p, keep, B, n, m = self._problem(lengths, degrees, caps, kv_caps, weights, ms)
+        per-problem worker counts of a ragged batch (degrees padded to [B, max m]); `ns` ([B] int):
+        per-problem item counts (lengths / weights padded to [B, max n])."""
+        p, keep, B, n, m = self._problem(lengths, degrees, caps, kv_caps, weights, ms, ns)
         obj = torch.empty(B, dtype=self.objective_dtype, device=self.device)
         st = torch.empty(B, dtype=torch.int32, device=self.device)
         s = (stream or torch.cuda.current_stream(self.device)).cuda_stream
@@ -150,10 +154,10 @@ class Placer:
         self._last = (keep, B, n, m)  # keep inputs alive until backtrack
         return obj, st
 
-    def objective(self, lengths, degrees, caps=None, kv_caps=None, stream=None, ms=None):
+    def objective(self, lengths, degrees, caps=None, kv_caps=None, stream=None, ms=None, ns=None):
         """Exact min-max optimum only (no partition), by the parametric search kernel (N3):
         bit-identical to solve()'s objective at O(m log n) probes per bisection step."""
-        p, keep, B, n, m = self._problem(lengths, degrees, caps, kv_caps, None, ms)
+        p, keep, B, n, m = self._problem(lengths, degrees, caps, kv_caps, None, ms, ns)
         obj = torch.empty(B, dtype=self.objective_dtype, device=self.device)
         st = torch.empty(B, dtype=torch.int32, device=self.device)
         s = (stream or torch.cuda.current_stream(self.device)).cuda_stream

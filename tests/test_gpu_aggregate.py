@@ -1,0 +1,75 @@
+"""GPU: short-trajectory aggregation on the device (K10, heddle_place_aggregate / _expand) and the
+ragged weighted solve of the aggregated batch, against oracle/aggregate.py
+and the weighted oracle DP, bit for bit; aggregated >= exact."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from inputs import workloads as wl
+from oracle.aggregate import aggregate as ora_aggregate, expand as ora_expand
+from paper_2603_28101_b200 import aggregate as agg_mod
+from paper_2603_28101_b200.placer import Placer
+from tests.parity import to_dev
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _build():
+    import __graft_entry__
+    __graft_entry__.build()
+
+
+@pytest.mark.parametrize("dtype", ["f32", "u32", "f64"])
+def test_device_aggregate_matches_oracle(dtype):
+    rng = np.random.default_rng(9)
+    B, n = 24, 400
+    rows = []
+    for b in range(B):
+        L = wl.presort(wl.coding_lengths(rng, n // 8, 8))
+        rows.append(L if dtype != "f32" else wl.predicted(rng, L))
+    Ls = np.stack([wl.presort(np.asarray(r, dtype=np.float64)) for r in rows])
+    npdt = {"f32": np.float32, "u32": np.uint32, "f64": np.float64}[dtype]
+    Ls = Ls.astype(npdt)
+    tdt = {"f32": torch.float32, "u32": torch.uint32, "f64": torch.float64}[dtype]
+    for thr, bucket in ((0.0, 4), (float(np.percentile(Ls, 50)), 8), (1e9, 3), (float(Ls.min()), 1)):
+        agg, w, st, na = agg_mod.aggregate(to_dev(Ls, tdt), thr, bucket)
+        torch.cuda.synchronize()
+        agg = agg.cpu().numpy() if dtype != "u32" else agg.cpu().view(torch.int32).numpy().view(np.uint32)
+        w, st, na = w.cpu().numpy(), st.cpu().numpy(), na.cpu().numpy()
+        for b in range(B):
+            oi, ow, ost = ora_aggregate(list(Ls[b]), thr, bucket)
+            k = na[b]
+            assert k == len(oi) and list(agg[b, :k]) == oi and list(w[b, :k]) == ow, (thr, bucket, b)
+            assert list(st[b, :k]) == ost[:-1] and st[b, n] == n
+
+
+@pytest.mark.parametrize("algo", ["scan", "valley"])
+def test_aggregated_ragged_solve_matches_weighted_oracle(algo):
+    """Rollout-shaped problems, aggregated on the device into a ragged batch (different n'),
+    solved with weights in one launch, expanded back: equal to the weighted oracle DP on
+    oracle/aggregate.py's items, and never better than the exact optimum."""
+    prof = wl.float_profile()
+    rng = np.random.default_rng(17)
+    B, n, m = 12, 512, 32
+    Ls = np.stack([wl.presort(wl.predicted(rng, wl.coding_lengths(rng, n // 8, 8))) for _ in range(B)])
+    deg = wl.sorted_degree_vectors(rng, B, m).astype(np.int32)
+    thr = float(np.percentile(Ls, 70))
+    agg, w, st, na = agg_mod.aggregate(to_dev(Ls), thr, 8)
+    pl = Placer.from_profile(prof, max_n=n, max_m=m, max_batch=B, algo=algo)
+    obj, status = pl.solve(agg, to_dev(deg), weights=w, ns=na)
+    bnd = pl.backtrack()
+    full = agg_mod.expand(bnd, st)
+    torch.cuda.synchronize()
+    obj, status, bnd, full = obj.cpu().numpy(), status.cpu().numpy(), bnd.cpu().numpy(), full.cpu().numpy()
+    for b in range(B):
+        oi, ow, ost = ora_aggregate(list(Ls[b]), thr, 8)
+        p = oracle.Problem(np.asarray(oi), prof.T, prof.F, prof.row_of(deg[b]), mode="f32", w=np.asarray(ow))
+        ref = oracle.solve(p)
+        assert status[b] == 0 and obj[b] == ref["opt"], (b, obj[b], ref["opt"])
+        assert np.array_equal(bnd[b], ref["bounds"]), b
+        assert list(full[b]) == ora_expand(list(ref["bounds"]), ost), b
+        exact = oracle.solve(oracle.Problem(Ls[b], prof.T, prof.F, prof.row_of(deg[b]), mode="f32"))
+        assert obj[b] >= exact["opt"]
+    pl.close()

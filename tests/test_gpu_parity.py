@@ -439,25 +439,6 @@ def test_weighted_random_tiny_exact(dtype, semiring):
     assert done > 50
 
 
-def test_aggregated_rollout_matches_weighted_oracle():
-    """The paper's aggregation heuristic on the rollout workload: aggregate, weighted GPU solve,
-    expand; equal to the oracle's weighted DP and never better than the exact optimum."""
-    from paper_2603_28101_b200.aggregate import aggregate_short, expand_boundaries
-    for prob in range(3):
-        b = wl.config_rollout(problem=prob)
-        L = b.lengths[0]
-        agg, w, st = aggregate_short(L, float(np.percentile(L, 70)), 8)
-        ab = wl.Batch("agg", agg.size, b.m, agg[None, :].astype(np.float32), b.degrees, b.profile,
-                      weights=w[None, :])
-        g = run_gpu(ab, keep_parents=True)
-        ref = oracle.solve(oracle.Problem.from_batch(ab, 0, mode="f32"), want_tables=True)
-        assert_exact(g, 0, ref, ab, "f32", "minmax", check_parents=True, tag=f"agg{prob}")
-        exact = oracle.solve(oracle.Problem.from_batch(b, 0, mode="f32"))
-        assert g["obj"][0] >= exact["opt"]
-        full = expand_boundaries(g["bounds"][0], st)
-        assert full[0] == 0 and full[-1] == b.n and np.all(np.diff(full) > 0)
-
-
 # ------------------------------------------------------------------ N3: objective-only parametric solver
 @pytest.mark.parametrize("dtype", ["u32", "f32", "f64"])
 def test_objective_parametric_random_tiny(dtype):
