@@ -27,6 +27,7 @@
  *               v = fmaf(L, G, dp).  MINMAX values are selections => exact
  *               w.r.t. the float32 emulation; <= 2^-23 relative vs FP64.
  *   HEDDLE_F64: G = T*F, cost = L*G, MINPLUS v = fma(L, G, dp), all double.
+ *   HEDDLE_F32X (MINPLUS only): G and cost as HEDDLE_F32, v = dp + (double)cost in double.
  *   HEDDLE_U32: integer profile; G = T*F exactly (must be < 2^32); cost =
  *               L*G exactly; MINMAX objective uint32, MINPLUS objective uint64.
  *               Range guard: max L * max G < 2^32 - 65536 and L <= 65535,
@@ -73,7 +74,11 @@ typedef enum {
   HEDDLE_E_NOMEM = 9           /* device or host allocation failed                                    */
 } heddle_status;
 
-typedef enum { HEDDLE_U32 = 0, HEDDLE_F32 = 1, HEDDLE_F64 = 2 } heddle_dtype;
+/* HEDDLE_F32X: float32 lengths and profile, costs fl32(L*fl32(T*F)) as in HEDDLE_F32, but min-plus
+ * sums accumulated in float64 (dp values and the objective are double): the relative error of a
+ * sum of m positive costs is then that of its terms (~2^-23), whatever m -- the FP32 sum of m =
+ * 256 terms can drift towards the 1e-6 tolerance of north_star.  MINPLUS only. */
+typedef enum { HEDDLE_U32 = 0, HEDDLE_F32 = 1, HEDDLE_F64 = 2, HEDDLE_F32X = 3 } heddle_dtype;
 typedef enum { HEDDLE_MINMAX = 0 /* Eq. 3, default */, HEDDLE_MINPLUS = 1 } heddle_semiring;
 
 /* config.flags */

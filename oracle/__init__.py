@@ -26,10 +26,10 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "heddle_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
-F64, F32EMU, U32 = 0, 1, 2
+F64, F32EMU, U32, F32X = 0, 1, 2, 3
 MINMAX, MINPLUS = 0, 1
 OK, INVALID, INFEASIBLE, TOO_LARGE = 0, 1, 3, 9
-MODE_OF = {"f64": F64, "f32": F32EMU, "u32": U32}
+MODE_OF = {"f64": F64, "f32": F32EMU, "u32": U32, "f32x": F32X}
 
 
 def build(force: bool = False) -> str:

@@ -34,6 +34,8 @@
  *    P:595 / P:605.  F32EMU mode emulates the float32 arithmetic the library
  *    documents: g = fl32(T*F), cost = fl32(L*g); MINPLUS v = fmaf(L, g, dp).
  *    U32 mode: exact integer arithmetic, g = T*F, cost = L*g (uint64).
+ *    F32X mode (the library's "F32 costs, FP64 min-plus sums"): the
+ *    cost as in F32EMU, MINPLUS v = prev + cost added in double.
  *  - R8 only the states that lie on a complete m-group partition are
  *    computed: layer j covers i in [j, n-m+j]; all others stay +inf.
  *
@@ -47,7 +49,7 @@
 #include <omp.h>
 #endif
 
-enum { ORA_F64 = 0, ORA_F32EMU = 1, ORA_U32 = 2 };
+enum { ORA_F64 = 0, ORA_F32EMU = 1, ORA_U32 = 2, ORA_F32X = 3 };
 enum { ORA_MINMAX = 0, ORA_MINPLUS = 1 };
 enum { ORA_OK = 0, ORA_INVALID = 1, ORA_INFEASIBLE = 3, ORA_TOO_LARGE = 9 };
 
@@ -113,7 +115,7 @@ static double group_cost_w(const ora_problem* p, const int64_t* Wp, const double
   double Fv = p->F[f_index(p, j, size)];
   if (p->mode == ORA_F64) {
     return (p->L[k] * p->T[d]) * Fv;                 /* R7: (L*T)*F */
-  } else if (p->mode == ORA_F32EMU) {
+  } else if (p->mode == ORA_F32EMU || p->mode == ORA_F32X) {
     float g = (float)p->T[d] * (float)Fv;             /* fl32(T*F)   */
     float c = (float)p->L[k] * g;                     /* fl32(L*g)   */
     return (double)c;

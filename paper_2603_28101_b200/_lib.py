@@ -13,7 +13,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("HEDDLE_PLACE_LIB") or os.path.join(_HERE, "libheddle_place.so")
 
 OK, E_INVALID, E_UNSORTED, E_INFEASIBLE, E_RANGE, E_UNKNOWN_DEGREE, E_STATE, E_CUDA, E_NCCL, E_NOMEM = range(10)
-U32, F32, F64 = 0, 1, 2
+U32, F32, F64, F32X = 0, 1, 2, 3
 MINMAX, MINPLUS = 0, 1
 KEEP_PARENTS = 0x1
 FORCE_BATCHED = 0x2
@@ -22,7 +22,7 @@ VALLEY = 0x8
 KERNELS = {"auto": 0, "batched": FORCE_BATCHED, "layered": FORCE_LAYERED}
 ALGOS = {"scan": 0, "valley": VALLEY}   # full scan of the splits (Eq. 3) / valley search (min-max, N3)
 
-DTYPES = {"u32": U32, "f32": F32, "f64": F64}
+DTYPES = {"u32": U32, "f32": F32, "f64": F64, "f32x": F32X}   # f32x: F32 costs, FP64 min-plus sums
 SEMIRINGS = {"minmax": MINMAX, "minplus": MINPLUS}
 
 # exported symbols declared in include/heddle_place.h (tests check the .so exports all of them)

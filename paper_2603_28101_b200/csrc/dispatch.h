@@ -22,8 +22,10 @@ using K8LFn = void (*)(hp::SolveArgs, int, hp::ValleyWs);
 using K8SFn = void (*)(hp::SolveArgs, int, hp::ValleyWs);
 
 // dt: heddle_dtype, sr: heddle_semiring
+// (HEDDLE_F32X exists only with MINPLUS; heddle_place_init rejects the other combination)
 #define HP_DISPATCH(NAME, ...)                                                                          \
-  (dt == HEDDLE_F32 ? (sr == HEDDLE_MINMAX ? NAME<HEDDLE_F32, HEDDLE_MINMAX>(__VA_ARGS__)               \
+  (dt == HEDDLE_F32X ? NAME<HEDDLE_F32X, HEDDLE_MINPLUS>(__VA_ARGS__)                                  \
+   : dt == HEDDLE_F32 ? (sr == HEDDLE_MINMAX ? NAME<HEDDLE_F32, HEDDLE_MINMAX>(__VA_ARGS__)             \
                                            : NAME<HEDDLE_F32, HEDDLE_MINPLUS>(__VA_ARGS__))             \
    : dt == HEDDLE_F64 ? (sr == HEDDLE_MINMAX ? NAME<HEDDLE_F64, HEDDLE_MINMAX>(__VA_ARGS__)             \
                                              : NAME<HEDDLE_F64, HEDDLE_MINPLUS>(__VA_ARGS__))           \

@@ -131,9 +131,9 @@ struct heddle_place_ctx {
 
 namespace {
 
-size_t elem_size(int dtype) { return dtype == HEDDLE_F64 ? 8 : 4; }
+size_t elem_size(int dtype) { return dtype == HEDDLE_F64 ? 8 : 4; }   // lengths / profile / cost table
 size_t dp_elem_size(int dtype, int semiring) {
-  return (dtype == HEDDLE_F64 || (dtype == HEDDLE_U32 && semiring == HEDDLE_MINPLUS)) ? 8 : 4;
+  return (dtype == HEDDLE_F64 || dtype == HEDDLE_F32X || (dtype == HEDDLE_U32 && semiring == HEDDLE_MINPLUS)) ? 8 : 4;
 }
 
 struct DeviceGuard {
@@ -152,6 +152,7 @@ template <int DT, int SR> int k3_smem_t(int kc) { return K3Smem<DT, SR>(kc).tota
 int k3_smem(int dt, int sr, int kc) { return HP_DISPATCH(k3_smem_t, kc); }
 
 int k2_smem(int dt, int sr, int n, int m, bool kv, bool w = false) {
+  if (dt == HEDDLE_F32X) return K2Smem<HEDDLE_F32X, HEDDLE_MINPLUS>(n, m, kv, w).total;
   if (dt == HEDDLE_F32) return sr == HEDDLE_MINMAX ? K2Smem<HEDDLE_F32, HEDDLE_MINMAX>(n, m, kv, w).total : K2Smem<HEDDLE_F32, HEDDLE_MINPLUS>(n, m, kv, w).total;
   if (dt == HEDDLE_F64) return sr == HEDDLE_MINMAX ? K2Smem<HEDDLE_F64, HEDDLE_MINMAX>(n, m, kv, w).total : K2Smem<HEDDLE_F64, HEDDLE_MINPLUS>(n, m, kv, w).total;
   return sr == HEDDLE_MINMAX ? K2Smem<HEDDLE_U32, HEDDLE_MINMAX>(n, m, kv, w).total : K2Smem<HEDDLE_U32, HEDDLE_MINPLUS>(n, m, kv, w).total;
@@ -532,7 +533,7 @@ heddle_status solve_layered(heddle_place_ctx* x, SolveArgs& a, bool kp, bool kv,
     }
     x->xbuf_bytes = slab * des;
   }
-  const ncclDataType_t nt = dt == HEDDLE_F32 ? ncclFloat32 : dt == HEDDLE_F64 ? ncclFloat64
+  const ncclDataType_t nt = dt == HEDDLE_F32 ? ncclFloat32 : (dt == HEDDLE_F64 || dt == HEDDLE_F32X) ? ncclFloat64
                             : (sr == HEDDLE_MINMAX ? ncclUint32 : ncclUint64);
   const dim3 pg((unsigned)std::min<int64_t>((slab / B + 255) / 256, 1024), B);
   const dim3 ug((unsigned)std::min<int64_t>((slab * world / B + 255) / 256, 2048), B);
@@ -722,7 +723,8 @@ heddle_status heddle_place_init(const heddle_place_config* c, heddle_place_ctx**
   if (!out) return HEDDLE_E_INVALID;
   *out = nullptr;
   if (!c || !c->degrees || !c->T || !c->F) return HEDDLE_E_INVALID;
-  if (c->dtype < HEDDLE_U32 || c->dtype > HEDDLE_F64) return HEDDLE_E_INVALID;
+  if (c->dtype < HEDDLE_U32 || c->dtype > HEDDLE_F32X) return HEDDLE_E_INVALID;
+  if (c->dtype == HEDDLE_F32X && c->semiring != HEDDLE_MINPLUS) return HEDDLE_E_INVALID;   // nothing to accumulate
   if (c->semiring != HEDDLE_MINMAX && c->semiring != HEDDLE_MINPLUS) return HEDDLE_E_INVALID;
   if ((c->flags & HEDDLE_VALLEY) && c->semiring != HEDDLE_MINMAX) return HEDDLE_E_INVALID;   // no valley in a sum
   if (c->max_n < 1 || c->max_m < 1 || c->max_batch < 1 || c->num_degrees < 1 || c->s_max < 1) return HEDDLE_E_INVALID;
@@ -734,7 +736,7 @@ heddle_status heddle_place_init(const heddle_place_config* c, heddle_place_ctx**
   }
   double gmax = 0;
   uint32_t lmax = 0;
-  if (c->dtype == HEDDLE_F32) {
+  if (c->dtype == HEDDLE_F32 || c->dtype == HEDDLE_F32X) {
     if (!check_profile<float>(c, &gmax)) return HEDDLE_E_RANGE;
   } else if (c->dtype == HEDDLE_F64) {
     if (!check_profile<double>(c, &gmax)) return HEDDLE_E_RANGE;
@@ -802,7 +804,8 @@ heddle_status heddle_place_init(const heddle_place_config* c, heddle_place_ctx**
        cudaMemcpy(dF, c->F, es * (size_t)x->D * c->s_max, cudaMemcpyHostToDevice) == cudaSuccess;
   if (ok) {
     dim3 grid((x->gstride + 255) / 256, x->D);
-    if (c->dtype == HEDDLE_F32) k1_cost_tables<HEDDLE_F32><<<grid, 256>>>(dT, dF, x->D, c->s_max, x->gstride, x->d_gtab);
+    if (c->dtype == HEDDLE_F32 || c->dtype == HEDDLE_F32X)
+      k1_cost_tables<HEDDLE_F32><<<grid, 256>>>(dT, dF, x->D, c->s_max, x->gstride, x->d_gtab);
     else if (c->dtype == HEDDLE_F64) k1_cost_tables<HEDDLE_F64><<<grid, 256>>>(dT, dF, x->D, c->s_max, x->gstride, x->d_gtab);
     else k1_cost_tables<HEDDLE_U32><<<grid, 256>>>(dT, dF, x->D, c->s_max, x->gstride, x->d_gtab);
     x->launches++;
@@ -919,7 +922,7 @@ static heddle_status solve_impl(heddle_place_ctx* x, const heddle_place_problem*
   const bool valley = (x->flags & HEDDLE_VALLEY) != 0;
   const int smem2 = valley ? k8_smem(x->dtype, p->n, p->m, kv, wt) : k2_smem(x->dtype, x->semiring, p->n, p->m, kv, wt);
   const bool fits = smem2 <= (valley ? x->k8_smem_max : x->k2_smem_max);
-  const bool wide = (x->dtype == HEDDLE_F64) || (x->dtype == HEDDLE_U32 && x->semiring == HEDDLE_MINPLUS);
+  const bool wide = dp_elem_size(x->dtype, x->semiring) == 8;
   const bool ragged = p->ms != nullptr || p->ns != nullptr;   // per-problem sizes: one-CTA-per-problem kernels only
   const bool layered = !ragged && !per_problem_kernel(x, p->n, p->m, p->B, kv, wt);
   if (!layered && !fits) return HEDDLE_E_INVALID;   // n too large for the one-CTA-per-problem kernel
@@ -1410,7 +1413,7 @@ heddle_status heddle_place_aggregate(int32_t dtype, const void* lengths, int64_t
       lengths_stride < 0 || std::isnan(threshold))
     return HEDDLE_E_INVALID;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (dtype == HEDDLE_F32)
+  if (dtype == HEDDLE_F32 || dtype == HEDDLE_F32X)
     k10_aggregate<float><<<B, 128, 0, s>>>(static_cast<const float*>(lengths), lengths_stride, n, threshold, bucket,
                                            static_cast<float*>(agg_lengths_out), weights_out, starts_out, n_out);
   else if (dtype == HEDDLE_F64)
@@ -1482,7 +1485,8 @@ heddle_status heddle_place_anneal(heddle_place_ctx* x, const heddle_place_anneal
   sa.trace_c = O->trace;
   sa.accepted = O->accepted;
   sa.obj = obj;
-  sa.obj_kind = x->dtype == HEDDLE_F32 ? 0 : x->dtype == HEDDLE_F64 ? 1 : (x->semiring == HEDDLE_MINPLUS ? 3 : 2);
+  sa.obj_kind = x->dtype == HEDDLE_F32 ? 0 : (x->dtype == HEDDLE_F64 || x->dtype == HEDDLE_F32X) ? 1
+              : (x->semiring == HEDDLE_MINPLUS ? 3 : 2);
   std::vector<int> hdeg(x->prof_degrees);
   std::sort(hdeg.begin(), hdeg.end(), std::greater<int>());
   if (cudaMemcpyAsync(deg_desc, hdeg.data(), 4 * hdeg.size(), cudaMemcpyHostToDevice, s) != cudaSuccess ||

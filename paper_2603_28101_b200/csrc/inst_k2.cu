@@ -17,6 +17,7 @@ K2Fn pick_k2(bool kp, bool kv, bool w) {
 }
 
 K2Fn k2_for(int dt, int sr, bool kp, bool kv, bool w) {
+  if (dt == HEDDLE_F32X) return pick_k2<HEDDLE_F32X, HEDDLE_MINPLUS>(kp, kv, w);
   if (dt == HEDDLE_F32) return sr == HEDDLE_MINMAX ? pick_k2<HEDDLE_F32, HEDDLE_MINMAX>(kp, kv, w) : pick_k2<HEDDLE_F32, HEDDLE_MINPLUS>(kp, kv, w);
   if (dt == HEDDLE_F64) return sr == HEDDLE_MINMAX ? pick_k2<HEDDLE_F64, HEDDLE_MINMAX>(kp, kv, w) : pick_k2<HEDDLE_F64, HEDDLE_MINPLUS>(kp, kv, w);
   return sr == HEDDLE_MINMAX ? pick_k2<HEDDLE_U32, HEDDLE_MINMAX>(kp, kv, w) : pick_k2<HEDDLE_U32, HEDDLE_MINPLUS>(kp, kv, w);

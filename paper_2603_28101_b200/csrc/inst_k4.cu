@@ -19,6 +19,7 @@ K4Fn pick_k4c(bool kv, bool w) {
 
 
 K4Fn k4_for(int dt, int sr, bool kv, bool w) {
+  if (dt == HEDDLE_F32X) return pick_k4<HEDDLE_F32X, HEDDLE_MINPLUS>(kv, w);
   if (dt == HEDDLE_F32) return sr == HEDDLE_MINMAX ? pick_k4<HEDDLE_F32, HEDDLE_MINMAX>(kv, w) : pick_k4<HEDDLE_F32, HEDDLE_MINPLUS>(kv, w);
   if (dt == HEDDLE_F64) return sr == HEDDLE_MINMAX ? pick_k4<HEDDLE_F64, HEDDLE_MINMAX>(kv, w) : pick_k4<HEDDLE_F64, HEDDLE_MINPLUS>(kv, w);
   return sr == HEDDLE_MINMAX ? pick_k4<HEDDLE_U32, HEDDLE_MINMAX>(kv, w) : pick_k4<HEDDLE_U32, HEDDLE_MINPLUS>(kv, w);

@@ -71,6 +71,20 @@ struct Tr<HEDDLE_F64, HEDDLE_MINPLUS> {
   __device__ static __forceinline__ D zero() { return 0.0; }
 };
 
+// ---- F32X: F32 costs, FP64 min-plus accumulation -------------------------------
+template <>
+struct Tr<HEDDLE_F32X, HEDDLE_MINPLUS> {
+  using L = float;
+  using G = float;
+  using D = double;
+  __device__ static __forceinline__ D inf() { return __longlong_as_double(0x7ff0000000000000ll); }
+  __device__ static __forceinline__ G gpad() { return __int_as_float(0x7f800000); }
+  __device__ static __forceinline__ D comb(D dp, L l, G g) { return __dadd_rn(dp, (double)__fmul_rn(l, g)); }
+  __device__ static __forceinline__ D vmin(D a, D b) { return fmin(a, b); }
+  __device__ static __forceinline__ D norm(D v) { return v; }
+  __device__ static __forceinline__ D zero() { return 0.0; }
+};
+
 // ---- U32 (integer-quantised costs, bit-exact mode) ------------------------------
 // Padding entries of the G table are 0xFFFFFFFF.  In MINMAX the 32-bit product
 // L * 0xFFFFFFFF wraps to 2^32 - L >= 2^32 - 65535 (L <= 65535 by the range

@@ -16,8 +16,8 @@ import torch
 
 from . import _lib as C
 
-_TORCH_DT = {C.U32: torch.uint32, C.F32: torch.float32, C.F64: torch.float64}
-_NP_DT = {C.U32: np.uint32, C.F32: np.float32, C.F64: np.float64}
+_TORCH_DT = {C.U32: torch.uint32, C.F32: torch.float32, C.F64: torch.float64, C.F32X: torch.float32}
+_NP_DT = {C.U32: np.uint32, C.F32: np.float32, C.F64: np.float64, C.F32X: np.float32}
 
 
 def _ptr(t):
@@ -98,6 +98,8 @@ class Placer:
     def objective_dtype(self):
         if self.dtype == C.U32 and self.semiring == C.MINPLUS:
             return torch.uint64
+        if self.dtype == C.F32X:
+            return torch.float64
         return _TORCH_DT[self.dtype]
 
     @property

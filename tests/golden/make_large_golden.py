@@ -1,6 +1,8 @@
 #!/usr/bin/env python
 """Writes tests/golden/large_f32.npz: the CPU oracle's solution of BASELINE.json configs[4]
-(one n = 65536 coding-like instance into m = 256 workers, FP32 costs, Eq. 3 min-max).
+(one n = 65536 coding-like instance into m = 256 workers, FP32 costs, Eq. 3 min-max); with
+--mode f64 --semiring minplus --out tests/golden/large_f64_minplus.npz the FP64 min-plus solution
+of the same instance (the reference for the FP64-accumulated min-plus mode).
 
 Calls only oracle/ (the plain FP64-emulating-FP32 DP of P:592-616, ora_solve_threads: the columns
 of each layer shared over OpenMP threads, arithmetic and k order unchanged) and the seeded input
@@ -55,9 +57,12 @@ def main():
     ap.add_argument("--n", type=int, default=65536)
     ap.add_argument("--m", type=int, default=256)
     ap.add_argument("--out", default=OUT)
+    ap.add_argument("--mode", default="f32", help="oracle arithmetic: f32 (F32 emulation, the default file), f64")
+    ap.add_argument("--semiring", default="minmax", choices=["minmax", "minplus"])
     args = ap.parse_args()
     batch = wl.config_large(n=args.n, m=args.m)
-    p = oracle.Problem.from_batch(batch, 0, mode="f32")
+    p = oracle.Problem.from_batch(batch, 0, mode=args.mode,
+                                  semiring=oracle.MINMAX if args.semiring == "minmax" else oracle.MINPLUS)
     t = time.time()
     ref = oracle.solve(p, want_tables=True, threads=args.threads)
     dt = time.time() - t
@@ -69,7 +74,8 @@ def main():
         dp=ref["dp"][qj, qi], parent=ref["parent"][qj, qi].astype(np.int32),
         n=np.int32(n), m=np.int32(m),
         lengths_sha256=np.array(hashlib.sha256(np.ascontiguousarray(batch.lengths).tobytes()).hexdigest()),
-        oracle_seconds=np.float64(dt), threads=np.int32(args.threads))
+        oracle_seconds=np.float64(dt), threads=np.int32(args.threads), mode=np.array(args.mode),
+        semiring=np.array(args.semiring))
     print(f"wrote {args.out}: opt {ref['opt']!r}, {qj.size} sampled states, oracle {dt:.0f} s on "
           f"{args.threads} threads")
 

@@ -17,7 +17,7 @@ from paper_2603_28101_b200.placer import Placer
 
 REL_TOL = 1e-6  # north_star: "objective within 1e-6 relative" for FP32/FP64 costs
 SR = {"minmax": oracle.MINMAX, "minplus": oracle.MINPLUS}
-TDT = {"u32": torch.uint32, "f32": torch.float32, "f64": torch.float64}
+TDT = {"u32": torch.uint32, "f32": torch.float32, "f64": torch.float64, "f32x": torch.float32}
 
 
 def to_dev(a, dt=None):

@@ -73,3 +73,30 @@ def test_aggregated_ragged_solve_matches_weighted_oracle(algo):
         exact = oracle.solve(oracle.Problem(Ls[b], prof.T, prof.F, prof.row_of(deg[b]), mode="f32"))
         assert obj[b] >= exact["opt"]
     pl.close()
+
+
+@pytest.mark.parametrize("n,m,kernel", [(2000, 12, "layered"), (20000, 8, "auto")])
+def test_weighted_layered_valley_matches_oracle(n, m, kernel):
+    """Weights on the per-layer valley kernel (K8L): forced at n = 2000, and chosen by the
+    dispatcher at n = 20000 (beyond one CTA's shared memory); bit-exact against the weighted
+    oracle DP on device-aggregated items, with mixed degrees and a size cap."""
+    prof = wl.float_profile()
+    rng = np.random.default_rng(23 + n)
+    L = wl.presort(wl.predicted(rng, wl.coding_lengths(rng, n // 8, 8)))
+    agg, w, st, na = agg_mod.aggregate(to_dev(L[None, :]), float(np.percentile(L, 60)), 4)
+    k = int(na.cpu()[0])
+    A = agg[:, :k].contiguous()
+    Wt = w[:, :k].contiguous()
+    deg = wl.sorted_degree_vectors(rng, 1, m).astype(np.int32)
+    caps = np.full((1, m), -1, np.int32)
+    caps[0, -1] = n // 3
+    pl = Placer.from_profile(prof, max_n=n, max_m=m, max_batch=1, algo="valley", kernel=kernel)
+    obj, stt = pl.solve(A, to_dev(deg), caps=to_dev(caps), weights=Wt)
+    bnd = pl.backtrack()
+    torch.cuda.synchronize()
+    p = oracle.Problem(A.cpu().numpy()[0], prof.T, prof.F, prof.row_of(deg[0]), mode="f32",
+                       w=Wt.cpu().numpy()[0], caps=caps[0])
+    ref = oracle.solve(p, threads=8)
+    assert int(stt.cpu()[0]) == 0 and float(obj.cpu()[0]) == ref["opt"]
+    assert np.array_equal(bnd.cpu().numpy()[0], ref["bounds"])
+    pl.close()

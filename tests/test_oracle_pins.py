@@ -82,6 +82,26 @@ def test_capacity_golden_cases():
             assert oracle.parametric_opt(p)["opt"] == case["opt"], case["cite"]
 
 
+def test_f32x_mode_sums_float32_costs_in_double():
+    """F32X: every candidate is the double sum of float32 costs fl32(L*fl32(T*F)); on
+    m = n (one item per worker, P4's closed form for the partition) the objective is that sum,
+    computed here with numpy's float32 products and a float64 accumulation."""
+    rng = np.random.default_rng(12)
+    for _ in range(20):
+        n = int(rng.integers(2, 40))
+        L = np.sort(rng.uniform(1, 5000, size=n).astype(np.float32))[::-1].astype(np.float64)
+        T = float(np.float32(rng.uniform(0.01, 0.1)))
+        F = [1.0]
+        p = oracle.Problem(L, [T], [F], [0] * n, mode="f32x", semiring=oracle.MINPLUS)
+        r = oracle.solve(p)
+        g = np.float32(T) * np.float32(1.0)
+        want = float(np.sum((L.astype(np.float32) * g).astype(np.float64)))
+        assert r["status"] == oracle.OK and list(r["bounds"]) == list(range(n + 1))
+        assert abs(r["opt"] - want) <= 1e-12 * want, (r["opt"], want)
+        f32 = oracle.solve(oracle.Problem(L, [T], [F], [0] * n, mode="f32", semiring=oracle.MINPLUS))
+        assert abs(f32["opt"] - want) <= 1e-5 * want       # the float32 chain: same terms, float sums
+
+
 def test_infeasible_n_less_than_m():
     p = homog([5, 4], 1.0, [1.0], 3)
     assert oracle.solve(p)["status"] == oracle.INFEASIBLE          # S:296
