@@ -6,8 +6,10 @@ costs in makespan and saves in DP time, on the paper's call shapes -- configs[1]
 For each threshold (a percentile of the lengths) and the SPEC default bucket 8: aggregate on the
 device (K10), solve the ragged weighted batch, and compare with the exact DP of the same problem:
   delta = aggregated makespan / exact makespan - 1   (>= 0 by S:332)
-and the device time of each (CUDA events, median of --reps).  Both solves use the exact valley
-solver (HEDDLE_VALLEY); the scan gives the same makespans.
+and the device time of each (CUDA events, median of --reps; the aggregated time includes the
+aggregation and expansion kernels), for the O(n^2 m) scan -- the DP the paper's heuristic is for --
+and for the exact valley solver (HEDDLE_VALLEY).  One instance per call: the aggregated item count
+is read back and the items solved as an n'-item problem (a batch would pass ns instead).
     python bench/aggregation.py [--reps 5]
 """
 from __future__ import annotations
@@ -59,31 +61,36 @@ def main():
     for name, b in cfgs:
         L = torch.from_numpy(b.lengths).cuda()
         D = torch.from_numpy(b.degrees.astype(np.int32)).cuda()
-        pl = Placer.from_profile(b.profile, max_n=b.n, max_m=b.m, max_batch=1, algo="valley")
+        for algo in ("scan", "valley"):
+            if algo == "scan" and b.n > 8192:
+                continue   # the weighted scan needs one CTA per problem (n' too large here)
+            pl = Placer.from_profile(b.profile, max_n=b.n, max_m=b.m, max_batch=1, algo=algo)
 
-        def exact():
-            o, _ = pl.solve(L, D)
-            return o, pl.backtrack()
-        t_exact, (o_ex, _) = timed(exact)
-        ex = float(o_ex.cpu()[0])
-        for pct in (50, 70, 90):
-            thr = float(np.percentile(b.lengths[0], pct))
-
-            def aggregated():
+            def exact():
+                o, _ = pl.solve(L, D)
+                return o, pl.backtrack()
+            t_exact, (o_ex, _) = timed(exact)
+            ex = float(o_ex.cpu()[0])
+            for pct in (50, 70, 90):
+                thr = float(np.percentile(b.lengths[0], pct))
                 a, w, st, na = agg_mod.aggregate(L, thr, args.bucket)
-                o, s = pl.solve(a, D, weights=w, ns=na)
-                return o, s, agg_mod.expand(pl.backtrack(), st), na
-            t_agg, (o_ag, s_ag, full, na) = timed(aggregated)
-            ag = float(o_ag.cpu()[0])
-            fb = full.cpu().numpy()[0]
-            print(json.dumps({
-                "config": name, "n": b.n, "m": b.m, "threshold_percentile": pct, "threshold": thr,
-                "bucket": args.bucket, "items": int(na.cpu()[0]), "status": int(s_ag.cpu()[0]),
-                "exact_makespan": ex, "aggregated_makespan": ag, "delta": ag / ex - 1.0,
-                "us_exact": round(t_exact, 1), "us_aggregated": round(t_agg, 1),
-                "expanded_boundaries_ok": bool(fb[0] == 0 and fb[-1] == b.n and np.all(np.diff(fb) > 0))}),
-                flush=True)
-        pl.close()
+                k = int(na.cpu()[0])
+
+                def aggregated():
+                    a, w, st, _ = agg_mod.aggregate(L, thr, args.bucket)
+                    o, s = pl.solve(a[:, :k], D, weights=w[:, :k])
+                    return o, s, agg_mod.expand(pl.backtrack(), st)
+                t_agg, (o_ag, s_ag, full) = timed(aggregated)
+                ag = float(o_ag.cpu()[0])
+                fb = full.cpu().numpy()[0]
+                print(json.dumps({
+                    "config": name, "algo": algo, "n": b.n, "m": b.m, "threshold_percentile": pct,
+                    "threshold": thr, "bucket": args.bucket, "items": k, "status": int(s_ag.cpu()[0]),
+                    "exact_makespan": ex, "aggregated_makespan": ag, "delta": ag / ex - 1.0,
+                    "us_exact": round(t_exact, 1), "us_aggregated": round(t_agg, 1),
+                    "expanded_boundaries_ok": bool(fb[0] == 0 and fb[-1] == b.n and np.all(np.diff(fb) > 0))}),
+                    flush=True)
+            pl.close()
 
 
 if __name__ == "__main__":
