@@ -255,9 +255,11 @@ def cpu_baseline(sample=64):
 
 
 def latency_lines(dev, reps=20):
-    """Device latency of the paper's own call shapes (solve + backtrack, CUDA events on the
-    launching stream, median of `reps` after warm-up): configs[1] rollout, configs[2] TP sweep and
-    the paper's §6.2 size (n = 6400, m = 16; the paper quotes ~42 ms on its CPU)."""
+    """Latency of the paper's own call shapes, solve + backtrack: `us` = CUDA events around each
+    call through the Python binding (median of `reps`; includes the host time of the call), and
+    `device_us_graph` = the same pair captured as a CUDA graph and replayed back to back (device
+    time alone).  configs[1] rollout, configs[2] TP sweep and the paper's §6.2 size (n = 6400,
+    m = 16; the paper quotes ~42 ms on its CPU)."""
     import torch
     from inputs import workloads as wl
     from paper_2603_28101_b200.placer import Placer
@@ -292,8 +294,37 @@ def latency_lines(dev, reps=20):
                 tb.append(e[1].elapsed_time(e[2]) * 1e3)
             W = b.B * transitions(b.n, b.m)
             t = statistics.median([a + c for a, c in zip(ts, tb)])
+            # device time alone: the solve + backtrack pair captured once as a CUDA graph and replayed
+            # back to back (no host work between the kernels)
+            dev_us = None
+            try:
+                g = torch.cuda.CUDAGraph()
+                side = torch.cuda.Stream(dev)
+                side.wait_stream(stream)
+                with torch.cuda.stream(side):
+                    pl.solve(L, D)
+                    pl.backtrack()
+                    torch.cuda.synchronize()
+                    with torch.cuda.graph(g, stream=side):
+                        pl.solve(L, D)
+                        pl.backtrack()
+                torch.cuda.synchronize()
+                for _ in range(3):
+                    g.replay()
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for _ in range(reps):
+                    g.replay()
+                e1.record(stream)
+                torch.cuda.synchronize()
+                dev_us = e0.elapsed_time(e1) * 1e3 / reps
+                del g
+            except Exception as ex:   # capture unsupported on this path: report the event time only
+                dev_us = f"graph capture failed: {ex}"[:120]
             res[algo] = {"us": round(t, 1), "us_solve": round(statistics.median(ts), 1),
-                         "us_backtrack": round(statistics.median(tb), 1), "cells_per_s": W / (t * 1e-6)}
+                         "us_backtrack": round(statistics.median(tb), 1), "cells_per_s": W / (t * 1e-6),
+                         "device_us_graph": round(dev_us, 1) if isinstance(dev_us, float) else dev_us}
             pl.close()
         out[name] = res
     return out

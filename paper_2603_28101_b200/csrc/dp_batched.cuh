@@ -121,12 +121,20 @@ __device__ __forceinline__ void check_sweep(int kq, int iters, int R, int sdp_lo
 template <int DT, int SR>
 struct K2Smem {
   using T = Tr<DT, SR>;
-  int gOff, g2Off, lOff, d0Off, d1Off, kloOff, spOff, wpOff, rowOff, capOff, kvOff, total;
+  int gOff, g2Off, gbOff, g2bOff, lOff, d0Off, d1Off, kloOff, spOff, wpOff, rowOff, capOff, kvOff, total;
   __host__ __device__ K2Smem(int n, int m, bool kv, bool w = false) {
     int o = 0;
     auto take = [&](int bytes) { int at = o; o += (bytes + 15) & ~15; return at; };
-    gOff = take((int)sizeof(typename T::G) * align4(kGPad + n + kGTail + 1));
-    g2Off = take((int)sizeof(typename T::G) * align4(kGPad + n + kGTail + 1));   // sG2[t] = sG[t + 1]
+    auto take128 = [&](int bytes) { o = (o + 127) & ~127; return take(bytes); };
+    const int gb = (int)sizeof(typename T::G) * align4(kGPad + n + kGTail + 1);
+    // two copies of the layer's cost table (and of its one-shifted copy): column lanes 0-3 read
+    // copy A, lanes 4-7 copy B, whose base sits 16 bytes further in the 128-byte bank cycle.  The
+    // G windows of lanes cl and cl+4 (32 columns apart = 128 bytes) then fall in different 16-byte
+    // bank groups, so a warp's window loads are conflict-free (4 wavefronts, not 8).
+    gOff = take128(gb);
+    g2Off = take128(gb);   // sG2[t] = sG[t + 1]
+    gbOff = take128(gb + 16) + 16;
+    g2bOff = take128(gb + 16) + 16;
     lOff = take((int)sizeof(typename T::L) * align4(n + kLPad));
     d0Off = take((int)sizeof(typename T::D) * align4(n + kLPad));
     d1Off = take((int)sizeof(typename T::D) * align4(n + kLPad));
@@ -452,6 +460,8 @@ __global__ void __launch_bounds__(kK2Threads, (SR == HEDDLE_MINMAX && DT != HEDD
   const K2Smem<DT, SR> lay(N, M, KV, W);
   G* sG = reinterpret_cast<G*>(smem + lay.gOff);
   G* sG2 = reinterpret_cast<G*>(smem + lay.g2Off);
+  G* sGb = reinterpret_cast<G*>(smem + lay.gbOff);     // bank-skewed copies (column lanes 4-7)
+  G* sG2b = reinterpret_cast<G*>(smem + lay.g2bOff);
   L* sL = reinterpret_cast<L*>(smem + lay.lOff);
   D* const sdp0 = reinterpret_cast<D*>(smem + lay.d0Off);
   D* const sdp1 = reinterpret_cast<D*>(smem + lay.d1Off);
@@ -490,9 +500,10 @@ __global__ void __launch_bounds__(kK2Threads, (SR == HEDDLE_MINMAX && DT != HEDD
         const int s = t - kGPad;
         const G g = (s >= 1 && s <= hi) ? grow[s] : T::gpad();
         sG[t] = g;
-        if (t > 0) sG2[t - 1] = g;
+        sGb[t] = g;
+        if (t > 0) { sG2[t - 1] = g; sG2b[t - 1] = g; }
       }
-      if (tid == 0) sG2[kGPad + n + kGTail] = T::gpad();
+      if (tid == 0) { sG2[kGPad + n + kGTail] = T::gpad(); sG2b[kGPad + n + kGTail] = T::gpad(); }
     }
     if constexpr (KV) {
       const int64_t kvc = skv[j - 1];
@@ -595,7 +606,9 @@ __global__ void __launch_bounds__(kK2Threads, (SR == HEDDLE_MINMAX && DT != HEDD
         } else {
           check_sweep(kstart + kg * Q, Q / 4, kLaneCols, 0, align4(n + kLPad), 0, align4(kGPad + n + kGTail + 1),
                       kGPad + c);
-          sweep_slide<DT, SR, KP, KV, kLaneCols>(sL, prev, sG + kGPad + c, sG2 + kGPad + c, kstart + kg * Q, Q / 4,
+          const bool skew = cl >= kColLanes / 2;
+          sweep_slide<DT, SR, KP, KV, kLaneCols>(sL, prev, (skew ? sGb : sG) + kGPad + c, (skew ? sG2b : sG2) + kGPad + c,
+                                                 kstart + kg * Q, Q / 4,
                                                  acc, arg, klo);
         }
         // combine the kSplitLanes partial minima of each column (lowest split on ties)
