@@ -81,6 +81,8 @@ struct SolveArgs {
   int2* rowcap;            // [B][m] {profile row, cap} per worker, written by the K3/K5 prologue, or null
   const int32_t* ms;       // [B] per-problem worker count (ragged m, <= m) or null (= m); one-CTA kernels
   const int32_t* ns;       // [B] per-problem item count (ragged n, <= n) or null (= n); one-CTA kernels
+  int32_t* fbounds;        // [B][m+1] boundaries from K8's fused backtrack (every dp row kept in shared
+                           // memory: small problems, few of them), or null
 };
 
 // worker count of problem b (ragged batches: SA proposals of different sizes in one launch);

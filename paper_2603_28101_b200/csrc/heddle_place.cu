@@ -127,6 +127,8 @@ struct heddle_place_ctx {
   size_t sa_bytes = 0;
   cudaStream_t sa_stream = nullptr;           // capture stream of the per-iteration CUDA graph
   std::vector<int> prof_degrees;              // host copy of the profile's degrees
+  int32_t* d_fbounds = nullptr;               // [max_batch][max_m+1] K8 fused-backtrack boundaries
+  bool last_fused = false;
 };
 
 namespace {
@@ -681,6 +683,7 @@ void heddle_place_destroy(heddle_place_ctx* ctx) {
   cudaFree(ctx->d_status);
   cudaFree(ctx->d_stage);
   cudaFree(ctx->d_sa);
+  cudaFree(ctx->d_fbounds);
   if (ctx->sa_stream) cudaStreamDestroy(ctx->sa_stream);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->copy_done) cudaEventDestroy(ctx->copy_done);
@@ -972,7 +975,21 @@ static heddle_status solve_impl(heddle_place_ctx* x, const heddle_place_problem*
     if (st != HEDDLE_OK) return st;
     if (!layered) {
       const bool wide_cta = p->B < x->num_sms;
-      k8_for(x->dtype, kp, kv, wt, wide_cta)<<<p->B, wide_cta ? kK8ThreadsWide : kK8Threads, smem2, s>>>(a);
+      // few small problems: keep every dp row in shared memory and backtrack inside the kernel
+      // (the latency of the rollout-sized call; heddle_place_backtrack then only copies)
+      const size_t tab = dp_elem_size(x->dtype, x->semiring) * (size_t)(p->m + 1) * (p->n + 1);
+      const bool fused = wide_cta && !kp && (size_t)smem2 + tab <= (size_t)x->k8_smem_max;
+      int smem_launch = smem2;
+      if (fused) {
+        if (!x->d_fbounds && cudaMalloc(&x->d_fbounds, 4 * (size_t)x->max_batch * (x->max_m + 1)) != cudaSuccess) {
+          cudaGetLastError();
+          return HEDDLE_E_NOMEM;
+        }
+        if (cudaMemsetAsync(x->d_fbounds, 0xFF, 4 * (size_t)p->B * (p->m + 1), s) != cudaSuccess) return HEDDLE_E_CUDA;
+        a.fbounds = x->d_fbounds;
+        smem_launch = smem2 + (int)tab;
+      }
+      k8_for(x->dtype, kp, kv, wt, wide_cta)<<<p->B, wide_cta ? kK8ThreadsWide : kK8Threads, smem_launch, s>>>(a);
       x->launches++;
       if (cudaGetLastError() != cudaSuccess) return HEDDLE_E_CUDA;
     }
@@ -985,6 +1002,7 @@ static heddle_status solve_impl(heddle_place_ctx* x, const heddle_place_problem*
     if (st != HEDDLE_OK) return st;
   }
   x->last = a;
+  x->last_fused = a.fbounds != nullptr;
   x->last_kv = kv;
   x->last_w = wt;
   x->last_layered = layered;
@@ -1001,6 +1019,9 @@ heddle_status heddle_place_backtrack(heddle_place_ctx* x, int32_t* boundaries_ou
   DeviceGuard guard(x->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const SolveArgs& a = x->last;
+  if (x->last_fused && !parents_out)   // the valley kernel already walked the back-pointers
+    return cudaMemcpyAsync(boundaries_out, x->d_fbounds, 4 * (size_t)a.B * (a.m + 1), cudaMemcpyDeviceToDevice, s) ==
+                   cudaSuccess ? HEDDLE_OK : HEDDLE_E_CUDA;
   // few min-plus problems: a CTA per problem (the cost bound prunes little there, so the
   // lowest-argmin scan can cover tens of thousands of splits per layer at large n)
   if (a.B < x->num_sms && x->semiring == HEDDLE_MINPLUS)
