@@ -260,10 +260,8 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k8_valley(SolveArgs a) {
   int64_t* skv = reinterpret_cast<int64_t*>(smem + lay.kvOff);
   // fused backtrack (a.fbounds): every dp row of the problem, [m+1][n+1], after the carve-up
   D* stab = (a.fbounds && !KP) ? reinterpret_cast<D*>(smem + lay.total) : nullptr;
-  // last descent of row r in s_dl[r % 3]: found by layer r before its closing barrier, read by
-  // layer r + 1, reset by layer r + 2 (three slots: no slot is reset while still being read)
-  __shared__ int s_err, s_dl[3];
-  if (tid < 3) s_dl[tid] = -1;
+  __shared__ int s_err, s_dlast[2];
+  if (tid == 0) { s_dlast[0] = -1; s_dlast[1] = -1; }
   if (load_problem<DT, HEDDLE_MINMAX, KV, W, NT>(a, b, n, m, sL, srow, scap, skv, sSp, sWp, s_err) != 0) return;
   __syncthreads();
   D* gdp = reinterpret_cast<D*>(a.dpws) + (int64_t)b * (M + 1) * (N + 1);
@@ -286,13 +284,18 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k8_valley(SolveArgs a) {
       const int cap = scap[j - 1], hi = (cap >= 0 && cap < n) ? cap : n;
       for (int t = tid; t <= n; t += NT) sG[t] = (t >= 1 && t <= hi) ? grow[t] : T::gpad();
     }
-    if (restage) __syncthreads();
-    if (tid == 0) s_dl[(j + 1) % 3] = -1;                 // row j+1's slot (last read by layer j-1)
+    if (j == 1 && restage) __syncthreads();
     if (j > 1) {
-      // range minimum of row j-1 over its computed region [j-1, n-m+j-1]; its last descent was
-      // found by layer j-1 (row 1 never descends: dp[1][i] = L[0] * G_1(i) is non-decreasing)
-      const int plo = j - 1;
-      dl = s_dl[(j - 1) % 3];
+      // range minimum of row j-1 over its computed region [j-1, n-m+j-1]
+      const int plo = j - 1, phi = n - m + j - 1;
+      int myd = -1;
+      for (int t = plo + tid; t < phi; t += NT)
+        if (prev[t] > prev[t + 1]) myd = t;
+      myd = __reduce_max_sync(0xffffffffu, myd);
+      if ((tid & 31) == 0 && myd >= 0) atomicMax(&s_dlast[j & 1], myd);
+      __syncthreads();
+      dl = s_dlast[j & 1];
+      if (tid == 0) s_dlast[(j + 1) & 1] = -1;          // for layer j+1 (read after its barrier)
       if (dl >= 0) {
         scan_prefix = dl - plo < a.vscan;
         if (tid < 32) suffix_min_warp<T>(prev, plo, dl + 1, ssmd, tid);
@@ -317,7 +320,6 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k8_valley(SolveArgs a) {
                         W ? gtab + (int64_t)srow[j - 1] * a.gstride : sG, sSp, sWp,
                         W ? ((cap >= 0 && cap < a.gstride - 1) ? cap : a.gstride - 1) : n, KV ? skv[j - 1] : -1,
                         scan_prefix};
-    bool rescan = false;   // row j's descents must be found by a scan after the barrier
     if (j == 1) {   // dp[1][i] = L(tau_1) * T * F(i)
       for (int i = ilo + tid; i <= ihi; i += NT) {
         const D v = V.cost(0, i);
@@ -354,43 +356,15 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k8_valley(SolveArgs a) {
       const int per = (ns + NT - 1) / NT;
       const int r0 = s0 + tid * per, r1 = min(ihi, r0 + per - 1);
       int from = j - 1;
-      int myd = -1;          // last descent of row j among this thread's pairs
-      D last = T::inf();
       for (int i = r0; i <= r1; ++i) {
         int arg = -1, ks;
         const D v = V.template solve<KP>(j - 1, i, from, arg, ks);
         from = ks;
         cur[i] = v;
         if (KP) gpar[(int64_t)j * (n + 1) + i] = arg;
-        if (i > r0 && last > v) myd = i - 1;
-        last = v;
-      }
-      if (j < m) {   // row m is never read as a previous row
-        if (pre_hi < ilo) {
-          // every pair of row j lies in one run or straddles two: the pair (r1, r1 + 1) is checked
-          // with state r1 + 1 recomputed here (the same value its own thread finds), so the row's
-          // last descent is known at this layer's one barrier
-          if (r0 <= r1 && r1 < ihi) {
-            int arg = -1, ks;
-            const D v = V.template solve<false>(j - 1, r1 + 1, from, arg, ks);
-            if (last > v) myd = r1;
-          }
-          myd = __reduce_max_sync(0xffffffffu, myd);
-          if (lane == 0 && myd >= 0) atomicMax(&s_dl[j % 3], myd);
-        } else {
-          rescan = true;   // prefix states were computed warp by warp: scan the row after the barrier
-        }
       }
     }
     __syncthreads();
-    if (rescan) {   // (uniform: depends on the layer only)
-      int myd = -1;
-      for (int t = ilo + tid; t < ihi; t += NT)
-        if (cur[t] > cur[t + 1]) myd = t;
-      myd = __reduce_max_sync(0xffffffffu, myd);
-      if ((tid & 31) == 0 && myd >= 0) atomicMax(&s_dl[j % 3], myd);
-      __syncthreads();
-    }
     // the finished row to the workspace (coalesced) for the backtrack; -1 parents off the region
     for (int i = tid; i <= n; i += NT) {
       const bool in = (i >= ilo && i <= ihi);
@@ -408,7 +382,8 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k8_valley(SolveArgs a) {
     if (a.status_out) a.status_out[b] = st;
     reinterpret_cast<D*>(a.objective)[b] = obj;
   }
-  if (stab) {   // fused backtrack from the shared-memory table (K4's rule: lowest k reproducing the value)
+  if (stab) {   // fused backtrack from the shared-memory table: K4's rule, the lowest k in
+                // [lower bound, cur) whose candidate reproduces dp[j][cur] (R3)
     int32_t* out = a.fbounds + (int64_t)b * (M + 1);
     for (int q = m + 1 + tid; q <= M; q += NT) out[q] = -1;
     if (obj == T::inf()) {
@@ -416,12 +391,21 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k8_valley(SolveArgs a) {
       return;
     }
     __shared__ int s_found;
-    int cur_i = n;
+    // the cost rows come from sG, restaged unmasked when the profile row changes (degrees only grow
+    // walking back): the lower bound already excludes the groups over a cap.  Without caps the
+    // forward pass left worker m's row unmasked in sG.
+    int cur_i = n, staged = (W || a.caps) ? -1 : srow[m - 1];
     if (tid == 0) out[m] = n;
     for (int j = m; j >= 2; --j) {
+      if (!W && srow[j - 1] != staged) {
+        staged = srow[j - 1];
+        __syncthreads();
+        const G* grow = gtab + (int64_t)staged * a.gstride;
+        for (int t = tid; t <= n; t += NT) sG[t] = t >= 1 ? grow[t] : T::gpad();
+      }
       const D target = stab[(int64_t)j * (n + 1) + cur_i];
       const int lo = split_lower_bound<DT, KV>(a, b, j, cur_i, sSp, sWp);
-      const G* grow = gtab + (int64_t)srow[j - 1] * a.gstride;
+      const G* grow = W ? gtab + (int64_t)srow[j - 1] * a.gstride : sG;
       if (tid == 0) s_found = INT_MAX;
       __syncthreads();
       int mine = INT_MAX;
