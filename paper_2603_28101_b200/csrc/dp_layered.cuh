@@ -290,8 +290,8 @@ struct K3Smem {
     gLen = align4(kK3Cols + kc + kK3GPadLo + 16);
     lOff = take((int)sizeof(typename T::L) * (kc + kK3LPad));
     dOff = take((int)sizeof(typename T::D) * (kc + kK3LPad));
-    gOff = take((int)sizeof(typename T::G) * gLen);
-    g2Off = take((int)sizeof(typename T::G) * gLen);
+    gOff = take((int)sizeof(typename T::G) * (gLen + 16)) + 16 * (int)sizeof(typename T::G) / 2;
+    g2Off = take((int)sizeof(typename T::G) * (gLen + 16)) + 16 * (int)sizeof(typename T::G) / 2;
     total = o;
   }
 };
@@ -582,6 +582,20 @@ __device__ __forceinline__ void bulk_span(const G* src, int lo, int len, int ghi
   t1 = ee - lo;
 }
 
+// Elements [t0, t1) of a staged window G(lo + t), t in [0, len), copied by ONE bulk copy rounded
+// outward to 16-byte boundaries (t0 may be negative down to -(E-1), t1 may pass len by up to E-1):
+// every element of the window with s in [1, ghi] comes from the copy, and those it brings in with
+// s < 1 or s > ghi are overwritten with the padding after it lands (bulk_fixup).  Requires src + lo
+// on a 16-byte boundary (the row-padded copies gA / gB) and smem room for the overhang.
+template <class G>
+__device__ __forceinline__ void bulk_span_out(int lo, int len, int ghi, int& t0, int& t1) {
+  constexpr int E = 16 / (int)sizeof(G);
+  const int s_lo = max(lo, 1), s_hi = min(lo + len, ghi + 1);   // needed values: s in [s_lo, s_hi)
+  if (s_hi <= s_lo) { t0 = t1 = 0; return; }
+  t0 = ((s_lo - lo) / E) * E;                                    // lo + t0 aligned (lo is)
+  t1 = ((s_hi - lo + E - 1) / E) * E;
+}
+
 // Warp-wide spin: lane l waits until flag(l) >= target(l) (target 0: nothing to wait for), acquire
 // at system scope (peers publish over NVLink) or GPU scope; ~10 s timeout raises *err.
 __device__ __forceinline__ bool wait_flags_warp(const unsigned long long* flag, unsigned long long target, bool sys,
@@ -623,11 +637,25 @@ __global__ void __launch_bounds__(kK3Threads, sizeof(typename Tr<DT, SR>::D) == 
   __shared__ int64_t s_tile;
   __shared__ int s_flag;
   __shared__ __align__(8) unsigned long long s_mbar;   // bulk-copy completion (one phase per valid tile)
+  // the tile's metadata, fetched by thread 0 while the previous tile was finishing: a tile starts
+  // without a dependent global load (the next tile index is dequeued at the start of the current one)
+  __shared__ int4 s_tl;
+  __shared__ int2 s_rc;
+  __shared__ int s_valid;
   uint32_t mphase = 0;
   const int64_t ntiles = pa.nentries * B;
+  auto fetch_meta = [&](int64_t t) {   // thread 0
+    if (t >= ntiles) return;
+    const int4 q = pa.tiles[t / B];
+    const int bb = (int)(t % B);
+    s_tl = q;
+    s_rc = a.rowcap[(int64_t)bb * m + q.x - 1];
+    s_valid = a.status[bb] == HEDDLE_OK;
+  };
   if (tid == 0) {
     mbar_init(&s_mbar);
     s_tile = (int64_t)atomicAdd(pa.counter, 1ull);
+    fetch_meta(s_tile);
   }
   for (;;) {
     __syncthreads();
@@ -635,7 +663,11 @@ __global__ void __launch_bounds__(kK3Threads, sizeof(typename Tr<DT, SR>::D) == 
     if (tile >= ntiles) break;
     unsigned long long* tr = pa.trace ? pa.trace + 6 * tile : nullptr;
     if (tr && tid == 0) tr[0] = gtimer();
-    const int4 tl = pa.tiles[tile / B];
+    // dequeue the next tile now: the round trip overlaps this tile (deadlock-free: the smallest
+    // unfinished tile is always some CTA's current tile, and its dependencies are all smaller)
+    unsigned long long next = 0;
+    if (tid == 0) next = atomicAdd(pa.counter, 1ull);
+    const int4 tl = s_tl;
     const int b = (int)(tile % B);
     // {j, blk | nch << 16, k0, k1}: splits [k0, k1) of column block blk (nch chunks, <= kc each)
     const int j = tl.x, blk = tl.y & 0xffff, nch = tl.y >> 16, k0 = tl.z, k1 = tl.w;
@@ -645,8 +677,8 @@ __global__ void __launch_bounds__(kK3Threads, sizeof(typename Tr<DT, SR>::D) == 
     const int imaxb = min(c0 + kK3Cols - 1, imax_layer);
     // invalid problems compute nothing but still count and publish their blocks, so that the
     // number of arrivals every rank expects does not depend on device-side validation
-    const bool valid = a.status[b] == HEDDLE_OK;
-    const int2 rc = a.rowcap[(int64_t)b * m + j - 1];   // {profile row, cap} of worker j (prologue)
+    const bool valid = s_valid;
+    const int2 rc = s_rc;   // {profile row, cap} of worker j (prologue)
     const L* gL = reinterpret_cast<const L*>(a.lengths) + (int64_t)b * a.ls;
     const D* gprev = reinterpret_cast<const D*>(a.dpws) + ((int64_t)b * (m + 1) + (j - 1)) * (n + 1);
     D* gcur = reinterpret_cast<D*>(a.dpws) + ((int64_t)b * (m + 1) + j) * (n + 1);
@@ -657,15 +689,16 @@ __global__ void __launch_bounds__(kK3Threads, sizeof(typename Tr<DT, SR>::D) == 
     // ---- L and the G window do not depend on row j-1: bulk copies (TMA) of L[k0, k1), G(s0 + t)
     // and G(s0 + 1 + t) are issued by thread 0 and land while the dependency wait runs; threads
     // write only the +inf / pad elements around them
+    const int cap = rc.y;
+    const int ghi = (cap >= 0 && cap < n) ? cap : n;
+    int a0 = 0, a1 = 0, b0 = 0, b1 = 0;
     if (valid) {
-      const G* grow = reinterpret_cast<const G*>(a.gtab) + (int64_t)rc.x * a.gstride;
       const G* gA = reinterpret_cast<const G*>(pa.gA) + (int64_t)rc.x * pa.gsp;
       const G* gB = reinterpret_cast<const G*>(pa.gB) + (int64_t)rc.x * pa.gsp;
-      const int cap = rc.y;
-      const int ghi = (cap >= 0 && cap < n) ? cap : n;
-      int a0, a1, b0, b1;
-      bulk_span(gA, s0, gl, ghi, a0, a1);
-      bulk_span(gB, s0 + 1, gl, ghi, b0, b1);
+      // each window is one bulk copy rounded outward; outside it the window holds padding only,
+      // so the threads write constants (no global loads on the tile's critical path)
+      bulk_span_out<G>(s0, gl, ghi, a0, a1);
+      bulk_span_out<G>(s0 + 1, gl, ghi, b0, b1);
       const bool lbulk = kl > 0 && !(reinterpret_cast<uintptr_t>(gL + k0) & 15);
       if (tid == 0) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // after the last tile's generic accesses
@@ -676,14 +709,8 @@ __global__ void __launch_bounds__(kK3Threads, sizeof(typename Tr<DT, SR>::D) == 
       }
       for (int t = lbulk ? kl + tid : tid; t < kl + kK3LPad; t += kK3Threads) sL[t] = t < kl ? __ldg(gL + k0 + t) : (L)1;
       for (int t = tid; t < gl; t += kK3Threads) {
-        if (t < a0 || t >= a1) {
-          const int s = s0 + t;
-          sG[t] = (s >= 1 && s <= ghi) ? __ldg(grow + s) : T::gpad();
-        }
-        if (t < b0 || t >= b1) {
-          const int s = s0 + 1 + t;
-          sG2[t] = (s >= 1 && s <= ghi) ? __ldg(grow + s) : T::gpad();
-        }
+        if (t < a0 || t >= a1) sG[t] = T::gpad();
+        if (t < b0 || t >= b1) sG2[t] = T::gpad();
       }
     }
     if (tr && tid == 0) tr[1] = gtimer();
@@ -716,6 +743,15 @@ __global__ void __launch_bounds__(kK3Threads, sizeof(typename Tr<DT, SR>::D) == 
     if (valid) {
     mbar_wait(&s_mbar, mphase);   // the bulk copies of this tile (each thread observes completion)
     mphase ^= 1u;
+    // the copies' overhang: sizes < 1 (the triangle k >= i) and over the cap become padding
+    for (int t = a0 + tid; t < a1; t += kK3Threads) {
+      const int s = s0 + t;
+      if (s < 1 || s > ghi) sG[t] = T::gpad();
+    }
+    for (int t = b0 + tid; t < b1; t += kK3Threads) {
+      const int s = s0 + 1 + t;
+      if (s < 1 || s > ghi) sG2[t] = T::gpad();
+    }
     // row j-1 was produced by other CTAs / peers: read at L2, all loads in flight before the stores
     stage_batched<kK3Threads, sizeof(D) == 4 ? 9 : 4>(kl + kK3LPad, [&](int t) { return t < kl ? ld_cg(gprev + k0 + t) : T::inf(); },
                                  [&](int t, D v) { sdp[t] = v; });
@@ -751,11 +787,10 @@ __global__ void __launch_bounds__(kK3Threads, sizeof(typename Tr<DT, SR>::D) == 
       }
     }
     }   // valid
-    // ---- completion of the column block -> publish.  The next tile is dequeued here, so its
-    // round trip overlaps the fence instead of starting the next iteration.
-    unsigned long long next = 0;
+    // ---- completion of the column block -> publish.  The next tile's metadata is fetched here,
+    // so its loads overlap the fence instead of starting the next iteration.
     if (tr && tid == 0) tr[4] = gtimer();
-    if (tid == 0) next = atomicAdd(pa.counter, 1ull);
+    if (tid == 0) fetch_meta((int64_t)next);
     __threadfence();
     __syncthreads();
     const int64_t bidx = ((int64_t)j * B + b) * ncb + blk;
