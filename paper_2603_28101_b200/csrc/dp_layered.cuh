@@ -743,14 +743,14 @@ __global__ void __launch_bounds__(kK3Threads, sizeof(typename Tr<DT, SR>::D) == 
     if (valid) {
     mbar_wait(&s_mbar, mphase);   // the bulk copies of this tile (each thread observes completion)
     mphase ^= 1u;
-    // the copies' overhang: sizes < 1 (the triangle k >= i) and over the cap become padding
-    for (int t = a0 + tid; t < a1; t += kK3Threads) {
-      const int s = s0 + t;
-      if (s < 1 || s > ghi) sG[t] = T::gpad();
-    }
-    for (int t = b0 + tid; t < b1; t += kK3Threads) {
-      const int s = s0 + 1 + t;
-      if (s < 1 || s > ghi) sG2[t] = T::gpad();
+    // the copies' overhang (fewer than 4 elements at each end): sizes < 1 (the triangle k >= i)
+    // and over the cap become padding
+    if (tid < 8) {
+      const int t = tid < 4 ? a0 + tid : a1 - 8 + tid;
+      if (t >= a0 && t < a1 && (s0 + t < 1 || s0 + t > ghi)) sG[t] = T::gpad();
+    } else if (tid < 16) {
+      const int t = tid < 12 ? b0 + tid - 8 : b1 - 16 + tid;
+      if (t >= b0 && t < b1 && (s0 + 1 + t < 1 || s0 + 1 + t > ghi)) sG2[t] = T::gpad();
     }
     // row j-1 was produced by other CTAs / peers: read at L2, all loads in flight before the stores
     stage_batched<kK3Threads, sizeof(D) == 4 ? 9 : 4>(kl + kK3LPad, [&](int t) { return t < kl ? ld_cg(gprev + k0 + t) : T::inf(); },
