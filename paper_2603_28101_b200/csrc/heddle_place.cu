@@ -974,11 +974,16 @@ static heddle_status solve_impl(heddle_place_ctx* x, const heddle_place_problem*
     const heddle_status st = layered ? solve_valley_layered(x, a, kp, kv, s) : HEDDLE_OK;
     if (st != HEDDLE_OK) return st;
     if (!layered) {
-      const bool wide_cta = p->B < x->num_sms;
+      // 1024-thread CTAs when problems are fewer than SMs and large enough to keep the threads busy;
+      // a small single problem (the rollout config) runs faster on 128 threads: a few consecutive
+      // states per thread (galloping from the previous crossing) and cheap 4-warp barriers
+      int wide_min_n = 2048;
+      if (const char* e = std::getenv("HEDDLE_PLACE_K8_WIDE_MIN_N")) wide_min_n = std::atoi(e);   // tuning
+      const bool wide_cta = p->B < x->num_sms && p->n >= wide_min_n;
       // few small problems: keep every dp row in shared memory and backtrack inside the kernel
       // (the latency of the rollout-sized call; heddle_place_backtrack then only copies)
       const size_t tab = dp_elem_size(x->dtype, x->semiring) * (size_t)(p->m + 1) * (p->n + 1);
-      const bool fused = wide_cta && !kp && (size_t)smem2 + tab <= (size_t)x->k8_smem_max;
+      const bool fused = p->B < x->num_sms && !kp && (size_t)smem2 + tab <= (size_t)x->k8_smem_max;
       int smem_launch = smem2;
       if (fused) {
         if (!x->d_fbounds && cudaMalloc(&x->d_fbounds, 4 * (size_t)x->max_batch * (x->max_m + 1)) != cudaSuccess) {
