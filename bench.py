@@ -510,7 +510,10 @@ def run_cuda(args):
                 "identical_to_scan": same}
         if args.workload == "large":
             line["exchange"] = exchange
-        if nvl_all is not None:
+        if nvl_all is not None and min(min(r) for r in nvl_all) < 0:
+            line["nvlink"] = {"unavailable": "NVML NVLink throughput counters read N/A on this pool "
+                                             "(profiles/r02_nvlink_probe.json); see bench/rank0_ncu.sh"}
+        elif nvl_all is not None:
             row_bytes = 4 * (n_ + 1)
             line["nvlink"] = {
                 "tx_bytes_per_step_by_rank": [r[0] for r in nvl_all],

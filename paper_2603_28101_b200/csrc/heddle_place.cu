@@ -974,10 +974,9 @@ static heddle_status solve_impl(heddle_place_ctx* x, const heddle_place_problem*
     const heddle_status st = layered ? solve_valley_layered(x, a, kp, kv, s) : HEDDLE_OK;
     if (st != HEDDLE_OK) return st;
     if (!layered) {
-      // 1024-thread CTAs when problems are fewer than SMs and large enough to keep the threads busy;
-      // a small single problem (the rollout config) runs faster on 128 threads: a few consecutive
-      // states per thread (galloping from the previous crossing) and cheap 4-warp barriers
-      int wide_min_n = 2048;
+      // 1024-thread CTAs when problems are fewer than SMs (measured: 128-thread CTAs take the
+      // rollout solve from 104 to 148 us, the TP sweep from 0.37 to 1.29 ms)
+      int wide_min_n = 0;
       if (const char* e = std::getenv("HEDDLE_PLACE_K8_WIDE_MIN_N")) wide_min_n = std::atoi(e);   // tuning
       const bool wide_cta = p->B < x->num_sms && p->n >= wide_min_n;
       // few small problems: keep every dp row in shared memory and backtrack inside the kernel
