@@ -522,6 +522,7 @@ struct PersistArgs {
   const int4* tiles;               // [nentries] {j, blk, q, nch(blk)}; problems interleaved b-minor
   int64_t nentries;
   unsigned long long* counter;     // global tile counter (zeroed per solve)
+  int static_sched;                // 1: CTA c takes tiles c, c + grid, ... (no dequeue round trip)
   unsigned int* blk_done;          // [m+1][B][ncb] finished tiles per block (zeroed per solve)
   unsigned long long* ready;       // [m+1][B][ncb] publication counters of this rank (zeroed per solve)
   unsigned long long epoch;        // ready target (1: one publication per block per solve)
@@ -654,7 +655,7 @@ __global__ void __launch_bounds__(kK3Threads, sizeof(typename Tr<DT, SR>::D) == 
   };
   if (tid == 0) {
     mbar_init(&s_mbar);
-    s_tile = (int64_t)atomicAdd(pa.counter, 1ull);
+    s_tile = pa.static_sched ? (int64_t)blockIdx.x : (int64_t)atomicAdd(pa.counter, 1ull);
     fetch_meta(s_tile);
   }
   for (;;) {
@@ -663,7 +664,7 @@ __global__ void __launch_bounds__(kK3Threads, sizeof(typename Tr<DT, SR>::D) == 
     if (tile >= ntiles) break;
     unsigned long long* tr = pa.trace ? pa.trace + 6 * tile : nullptr;
     if (tr && tid == 0) tr[0] = gtimer();
-    unsigned long long next = 0;
+    unsigned long long next = pa.static_sched ? (unsigned long long)(tile + gridDim.x) : 0ull;
     const int4 tl = s_tl;
     const int b = (int)(tile % B);
     // {j, blk | nch << 16, k0, k1}: splits [k0, k1) of column block blk (nch chunks, <= kc each)
@@ -790,7 +791,7 @@ __global__ void __launch_bounds__(kK3Threads, sizeof(typename Tr<DT, SR>::D) == 
     // ready tile on the dependency chain could sit reserved behind a CTA's long current tile.)
     if (tr && tid == 0) tr[4] = gtimer();
     if (tid == 0) {
-      next = atomicAdd(pa.counter, 1ull);
+      if (!pa.static_sched) next = atomicAdd(pa.counter, 1ull);
       fetch_meta((int64_t)next);
     }
     __threadfence();

@@ -375,6 +375,7 @@ heddle_status solve_persistent(heddle_place_ctx* x, SolveArgs& a, cudaStream_t s
   pa.nch = x->d_nch;
   pa.nentries = x->tiles_n;
   pa.counter = x->d_ctr;
+  if (const char* e = std::getenv("HEDDLE_PLACE_K5_STATIC")) pa.static_sched = std::atoi(e);   // A/B
   pa.blk_done = x->d_blkdone;
   pa.ready = x->d_ready;
   pa.epoch = 1ull;
