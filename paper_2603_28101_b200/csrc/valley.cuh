@@ -416,6 +416,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k8_valley(SolveArgs a) {
       if ((tid & 31) == 0 && mine != INT_MAX) atomicMin(&s_found, mine);
       __syncthreads();
       cur_i = s_found;
+      __syncthreads();          // every thread has read s_found before thread 0 resets it
       if (cur_i == INT_MAX) {   // unreachable: the target is one of these candidates
         for (int q = tid; q <= m; q += NT) out[q] = -1;
         return;
