@@ -10,13 +10,15 @@
 //    and current dp rows, the layer's cost table G_j[s] = T_dj * F_dj(min(s,s_max))
 //    masked by the worker's cap and padded with +inf for s <= 0 (so the
 //    triangular k < i bound costs no instruction) -- 17 KB at n = 1024;
-//  * a warp owns 128 consecutive columns (4 per lane) and sweeps the split k
-//    warp-uniformly 4 at a time: dp[k..k+3] and L[k..k+3] are LDS.128
-//    broadcasts, and the lane's G window slides by 4 per step with ONE LDS.128
-//    (register window of 8, unrolled x2 so no register moves);
-//  * per transition: FMUL + FMNMX(max) + FMNMX(min) = 3 issue slots, the
-//    measured B200 ceiling (profiles/r01_alu_peaks.jsonl: FMNMX and FMUL issue at
-//    1/clk/SMSP, FMNMX3 at 1/2);
+//  * a warp task is 64 consecutive columns: 8 column lanes x 8 columns, 4 split
+//    lanes each sweeping a contiguous quarter of the split range 4 splits at a time;
+//    dp[k..k+3] and L[k..k+3] are LDS.128 broadcasts, and the lane's G window slides
+//    by 4 per step with one LDS.128 from the table and one from its one-shifted copy
+//    (column lanes 4-7 read bank-skewed copies of both);
+//  * per transition: half an FMUL2 (FMA pipe) + FMNMX (max) + half an FMNMX3 (min):
+//    the ALU pipe takes 2 cycles per FMNMX and per FMNMX3 warp instruction, so a
+//    warp-cell costs 3 ALU cycles -- the roofline (profiles/r01_alu_pipes_ncu.csv;
+//    the FMNMX row of r01_alu_peaks.jsonl is a compiler-fusion artifact, annotated);
 //  * the value pass keeps no argmin (the backtrack kernel recomputes the
 //    lowest-index argmin of the m states it needs); HEDDLE_KEEP_PARENTS
 //    switches to an inner loop with a strict-'<' argmin per transition;
