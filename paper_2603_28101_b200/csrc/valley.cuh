@@ -30,6 +30,7 @@
 #pragma once
 #include <climits>
 #include <cstdint>
+#include <type_traits>
 
 #include "backtrack.cuh"
 #include "dp_batched.cuh"
@@ -118,8 +119,8 @@ __device__ __forceinline__ void block_masks(const typename T::D* vals, int lo, i
 // The layer's group cost and the valley search, shared by the shared-memory (K8) and the
 // global-memory (K8L) kernels.  Pointers address one problem; sizes are item counts, or weight
 // sums with aggregation weights (R5).
-template <int DT, bool KV, bool W>
-struct Valley {
+template <int DT, bool KV, bool W, bool ROWPAD = false>
+struct Valley {   // ROWPAD: `grow` is the worker's row staged for every size 0..n, +inf past the cap
   using T = Tr<DT, HEDDLE_MINMAX>;
   using L = typename T::L;
   using G = typename T::G;
@@ -137,7 +138,7 @@ struct Valley {
   // normalised cost of items [k, i) on worker j (+inf when inadmissible)
   __device__ __forceinline__ D cost(int k, int i) const {
     const int s = W ? sWp[i] - sWp[k] : i - k;
-    const G g = s <= ghi ? grow[s] : T::gpad();
+    const G g = (ROWPAD || s <= ghi) ? grow[s] : T::gpad();
     D v;   // L * G in the DP kernels' rounding (Tr<>::comb with dp = 0; no max needed: L, G > 0)
     if constexpr (DT == HEDDLE_F32) v = __fmul_rn(sL[k], g);
     else if constexpr (DT == HEDDLE_F64) v = __dmul_rn(sL[k], g);
@@ -149,14 +150,19 @@ struct Valley {
   }
   // dp[j][i] over splits [lo, i-1]; `from` >= lo is a split before which the crossing cannot
   // lie (the previous state's k*); returns the value, the lowest argmin (if wanted) and k*.
-  template <bool ARG>
+  // MONO: row j-1 has no descent (dlast < 0), so every range minimum is the row's own value
+  template <bool ARG, bool MONO = false>
   __device__ __forceinline__ D solve(int lo, int i, int from, int& arg, int& kstar) const {
     const int hi = i - 1;
+    auto R = [&](int k, int e) -> D {
+      if constexpr (MONO) return rm.v[k];
+      else return rm(k, e);
+    };
     // the probes' values are kept: the answer min(rm(k*, hi), cost(k*-1, i)) is usually probed
     D rm_t = T::inf(), c_f = T::inf();
     bool have_cf = false;
     auto crossed = [&](int k) {
-      const D r = rm(k, hi), c = cost(k, i);
+      const D r = R(k, hi), c = cost(k, i);
       if (r >= c) { rm_t = r; return true; }
       c_f = c;
       return false;
@@ -178,7 +184,7 @@ struct Valley {
     }
     kstar = t;
     // rm_t / c_f hold the last crossed / not-crossed probe, which are t and f when probed
-    D v = (t <= hi) ? (have_rt ? rm_t : rm(t, hi)) : T::inf();
+    D v = (t <= hi) ? (have_rt ? rm_t : R(t, hi)) : T::inf();
     if (t > lo) v = T::vmin(v, have_cf && f == t - 1 ? c_f : cost(t - 1, i));
     if constexpr (ARG) {
       if (v == T::inf()) {
@@ -199,7 +205,7 @@ struct Valley {
           b0 = hi;                                // rm(kappa, hi) <= v
           while (b0 - a0 > 1) {
             const int mid = (a0 + b0) >> 1;
-            if (rm(kappa, mid) <= v) b0 = mid; else a0 = mid;
+            if (R(kappa, mid) <= v) b0 = mid; else a0 = mid;
           }
           arg = b0;
         }
@@ -316,7 +322,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k8_valley(SolveArgs a) {
       }
     }
     const int cap = scap[j - 1];
-    Valley<DT, KV, W> V{sL, RowMin<T>{prev, ssmd, smask, ssp, ssp + nb, nb, dl},
+    Valley<DT, KV, W, !W> V{sL, RowMin<T>{prev, ssmd, smask, ssp, ssp + nb, nb, dl},
                         W ? gtab + (int64_t)srow[j - 1] * a.gstride : sG, sSp, sWp,
                         W ? ((cap >= 0 && cap < a.gstride - 1) ? cap : a.gstride - 1) : n, KV ? skv[j - 1] : -1,
                         scan_prefix};
@@ -356,13 +362,16 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k8_valley(SolveArgs a) {
       const int per = (ns + NT - 1) / NT;
       const int r0 = s0 + tid * per, r1 = min(ihi, r0 + per - 1);
       int from = j - 1;
-      for (int i = r0; i <= r1; ++i) {
-        int arg = -1, ks;
-        const D v = V.template solve<KP>(j - 1, i, from, arg, ks);
-        from = ks;
-        cur[i] = v;
-        if (KP) gpar[(int64_t)j * (n + 1) + i] = arg;
-      }
+      auto run = [&](auto mono) {
+        for (int i = r0; i <= r1; ++i) {
+          int arg = -1, ks;
+          const D v = V.template solve<KP, decltype(mono)::value>(j - 1, i, from, arg, ks);
+          from = ks;
+          cur[i] = v;
+          if (KP) gpar[(int64_t)j * (n + 1) + i] = arg;
+        }
+      };
+      if (dl < 0) run(std::true_type{}); else run(std::false_type{});   // (uniform per layer)
     }
     __syncthreads();
     // the finished row to the workspace (coalesced) for the backtrack; -1 parents off the region
