@@ -496,7 +496,8 @@ __global__ void __launch_bounds__(32 * kK8LWarps, 4) k8l_layer(SolveArgs a, int 
         v = V.cost(0, i);
         arg = (v == T::inf()) ? -1 : 0;
       } else {
-        v = V.template solve<KP>(j - 1, i, from, arg, ks);
+        v = rm.dlast < 0 ? V.template solve<KP, true>(j - 1, i, from, arg, ks)   // monotone row j-1
+                         : V.template solve<KP>(j - 1, i, from, arg, ks);
         from = ks;
       }
       gdp[(int64_t)j * (n + 1) + i] = v;
