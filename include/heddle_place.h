@@ -135,9 +135,10 @@ typedef struct {
   const int32_t* weights;       /* [B][n] item weights >= 1 or NULL (= 1): an item stands for w  */
                                 /*   trajectories after short-trajectory aggregation; */
                                 /*   group size = sum of weights (R5); sum <= max_n (else the    */
-                                /*   problem's E_RANGE).  Scan: the one-CTA-per-problem kernel    */
-                                /*   (E_INVALID if n needs the layered scan); HEDDLE_VALLEY: one  */
-                                /*   CTA per problem or, for large n, the per-layer valley kernel */
+                                /*   problem's E_RANGE).  One CTA per problem while n fits shared */
+                                /*   memory, else the per-layer kernel (scan: K3 with the cost    */
+                                /*   gathered per cell; HEDDLE_VALLEY: K8L).  Not in split mode   */
+                                /*   (E_INVALID)                                                  */
   int64_t weights_stride;
   const int32_t* ms;            /* [B] per-problem worker count m_b in [1, m], or NULL (= m for all): a
                                  *   ragged batch, e.g. the simulated-annealing proposals of Alg. 2

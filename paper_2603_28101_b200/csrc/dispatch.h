@@ -36,7 +36,7 @@ K2Fn k2_for(int dt, int sr, bool kp, bool kv, bool w = false);   // inst_k2.cu
 K4Fn k4_for(int dt, int sr, bool kv, bool w);                     // inst_k4.cu
 K4Fn k4c_for(int dt, int sr, bool kv, bool w);
 K4QFn k4q_for(int dt, int sr, bool kv, bool w);
-K3Fn k3_for(int dt, int sr, bool kp, bool kv);                    // inst_k35.cu
+K3Fn k3_for(int dt, int sr, bool kp, bool kv, bool w = false);                    // inst_k35.cu
 KPro pro_for(int dt, int sr, bool kp, bool kv);
 K5Fn k5_for(int dt, int sr);
 K8Fn k8_for(int dt, bool kp, bool kv, bool w, bool wide);         // inst_k8.cu

@@ -338,6 +338,43 @@ __device__ __forceinline__ void sweep_weighted(const typename Tr<DT, SR>::L* __r
   }
 }
 
+// The same with the columns' weight prefixes given (K3: the tile stages its column and split
+// windows of Wp separately; sWk is indexed by the absolute split k).
+template <int DT, int SR, bool KP, bool MASKED, int R>
+__device__ __forceinline__ void sweep_weighted_w(const typename Tr<DT, SR>::L* __restrict__ sL,
+                                                 const typename Tr<DT, SR>::D* __restrict__ sdp,
+                                                 const int* __restrict__ sWk, const int (&wi)[R],
+                                                 const typename Tr<DT, SR>::G* __restrict__ grow, int ghi, int k,
+                                                 int iters, typename Tr<DT, SR>::D (&acc)[R], int (&arg)[R],
+                                                 const int (&klo)[R]) {
+  using T = Tr<DT, SR>;
+#pragma unroll 2
+  for (int t = 0; t < iters; ++t) {
+    typename T::D dpv[4];
+    typename T::L lv[4];
+    int wk[4];
+    ld4(sdp + k, dpv);
+    ld4(sL + k, lv);
+    ld4(sWk + k, wk);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int sz = wi[r] - wk[u];
+        const typename T::G g = (sz >= 1 && sz <= ghi) ? __ldg(grow + sz) : T::gpad();
+        typename T::D v = T::comb(dpv[u], lv[u], g);
+        if (MASKED) v = (k + u >= klo[r]) ? v : T::inf();
+        if (KP) {
+          if (v < acc[r]) { acc[r] = v; arg[r] = k + u; }
+        } else {
+          acc[r] = T::vmin(acc[r], v);
+        }
+      }
+    }
+    k += 4;
+  }
+}
+
 // ---------------- load + validate one problem into shared memory (K2 and K8): lengths sorted,
 // finite, positive; degrees known and sorted; per-worker profile row / cap / kv cap; token and
 // weight prefix sums (also written to the workspace for the backtrack).  Returns the problem's

@@ -283,8 +283,8 @@ __global__ void k3_row_fill(SolveArgs a, int j) {
 template <int DT, int SR>
 struct K3Smem {
   using T = Tr<DT, SR>;
-  int lOff, dOff, gOff, g2Off, total, gLen;
-  __host__ __device__ K3Smem(int kc) {
+  int lOff, dOff, gOff, g2Off, wkOff, wcOff, total, gLen;
+  __host__ __device__ K3Smem(int kc, bool w = false) {
     int o = 0;
     auto take = [&](int bytes) { int at = o; o += (bytes + 15) & ~15; return at; };
     gLen = align4(kK3Cols + kc + kK3GPadLo + 16);
@@ -292,11 +292,13 @@ struct K3Smem {
     dOff = take((int)sizeof(typename T::D) * (kc + kK3LPad));
     gOff = take((int)sizeof(typename T::G) * (gLen + 16)) + 16 * (int)sizeof(typename T::G) / 2;
     g2Off = take((int)sizeof(typename T::G) * (gLen + 16)) + 16 * (int)sizeof(typename T::G) / 2;
+    wkOff = w ? take(4 * (kc + kK3LPad)) : -1;   // weight prefixes of the tile's splits (R5)
+    wcOff = w ? take(4 * kK3Cols) : -1;           // and of its columns
     total = o;
   }
 };
 
-template <int DT, int SR, bool KP, bool KV>
+template <int DT, int SR, bool KP, bool KV, bool W = false>
 __global__ void __launch_bounds__(kK3Threads) k3_layer(LayerArgs la) {
   using T = Tr<DT, SR>;
   using L = typename T::L;
@@ -307,11 +309,13 @@ __global__ void __launch_bounds__(kK3Threads) k3_layer(LayerArgs la) {
   const int n = a.n, m = a.m, j = la.j, kc = la.kc;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int cl = lane & (kColLanes - 1), kg = lane / kColLanes;
-  const K3Smem<DT, SR> lay(kc);
+  const K3Smem<DT, SR> lay(kc, W);
   L* sL = reinterpret_cast<L*>(smem + lay.lOff);
   D* sdp = reinterpret_cast<D*>(smem + lay.dOff);
   G* sG = reinterpret_cast<G*>(smem + lay.gOff);
   G* sG2 = reinterpret_cast<G*>(smem + lay.g2Off);
+  int* sWk = W ? reinterpret_cast<int*>(smem + lay.wkOff) : nullptr;
+  int* sWc = W ? reinterpret_cast<int*>(smem + lay.wcOff) : nullptr;
   const int imax_layer = n - m + j;
   const int cbase = j & ~3;
   const int kstart = (j - 1) & ~3;
@@ -392,9 +396,14 @@ __global__ void __launch_bounds__(kK3Threads) k3_layer(LayerArgs la) {
       sdp[t] = in ? gprev[k] : T::inf();
       sL[t] = in ? gL[k] : (L)1;
     }
+    if constexpr (W) {   // Wp of the splits (beyond k1: huge, so every size there is < 1) and columns
+      const int32_t* wp = a.wpws + (int64_t)b * (n + 1);
+      for (int t = tid; t < kc + kK3LPad; t += kK3Threads) sWk[t] = k0 + t < k1 ? wp[k0 + t] : INT_MAX / 2;
+      for (int t = tid; t < kK3Cols; t += kK3Threads) sWc[t] = wp[min(c0 + t, n)];
+    }
     // G(s) for s in [s0, s0 + gLen], s0 = c0 - k1 - kK3GPadLo (== 1 mod 4: window alignment)
     const int s0 = c0 - k1 - kK3GPadLo;
-    for (int t = tid; t <= lay.gLen; t += kK3Threads) {
+    for (int t = tid; !W && t <= lay.gLen; t += kK3Threads) {
       const int s = s0 + t;
       const G g = (s >= 1 && s <= ghi) ? grow[s] : T::gpad();
       if (t < lay.gLen) sG[t] = g;
@@ -415,9 +424,18 @@ __global__ void __launch_bounds__(kK3Threads) k3_layer(LayerArgs la) {
         for (int r = 0; r < kLaneCols; ++r) klo[r] = la.klo[(int64_t)b * (n + 1) + min(max(c + r, j), imaxb)];
       }
       // shifted bases: sdpb[k] = sdp[k - k0]; gcol - k - 3 = &G(c - k - 3)
-      check_sweep(k0 + kg * Q - k0, Q / 4, kLaneCols, 0, kc + kK3LPad, 0, lay.gLen, c - s0 - k0);
-      sweep_slide<DT, SR, KP, KV, kLaneCols>(sL - k0, sdp - k0, sG + (c - s0), sG2 + (c - s0), k0 + kg * Q, Q / 4,
-                                             acc, arg, klo);
+      if constexpr (W) {   // group size Wp[i] - Wp[k]: G gathered per cell from the worker's row
+        const int ghi_w = (cap >= 0 && cap < a.gstride - 1) ? cap : a.gstride - 1;
+        int wi[kLaneCols];
+#pragma unroll
+        for (int r = 0; r < kLaneCols; ++r) wi[r] = sWc[c - c0 + r];
+        sweep_weighted_w<DT, SR, KP, KV, kLaneCols>(sL - k0, sdp - k0, sWk - k0, wi, grow, ghi_w, k0 + kg * Q, Q / 4,
+                                                    acc, arg, klo);
+      } else {
+        check_sweep(k0 + kg * Q - k0, Q / 4, kLaneCols, 0, kc + kK3LPad, 0, lay.gLen, c - s0 - k0);
+        sweep_slide<DT, SR, KP, KV, kLaneCols>(sL - k0, sdp - k0, sG + (c - s0), sG2 + (c - s0), k0 + kg * Q, Q / 4,
+                                               acc, arg, klo);
+      }
 #pragma unroll
       for (int off = kColLanes; off < 32; off <<= 1) {
 #pragma unroll

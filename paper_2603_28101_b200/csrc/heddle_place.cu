@@ -150,8 +150,8 @@ struct DeviceGuard {
   }
 };
 
-template <int DT, int SR> int k3_smem_t(int kc) { return K3Smem<DT, SR>(kc).total; }
-int k3_smem(int dt, int sr, int kc) { return HP_DISPATCH(k3_smem_t, kc); }
+template <int DT, int SR> int k3_smem_t(int kc, bool w) { return K3Smem<DT, SR>(kc, w).total; }
+int k3_smem(int dt, int sr, int kc, bool w = false) { return HP_DISPATCH(k3_smem_t, kc, w); }
 
 int k2_smem(int dt, int sr, int n, int m, bool kv, bool w = false) {
   if (dt == HEDDLE_F32X) return K2Smem<HEDDLE_F32X, HEDDLE_MINPLUS>(n, m, kv, w).total;
@@ -252,7 +252,8 @@ bool per_problem_kernel(const heddle_place_ctx* x, int n, int m, int B, bool kv,
   if (x->split_world > 1) return false;
   if (x->flags & HEDDLE_VALLEY)   // K8 whenever the problem fits shared memory, else K8L
     return !(x->flags & HEDDLE_FORCE_LAYERED) && k8_smem(x->dtype, n, m, kv, wt) <= x->k8_smem_max;
-  if (wt || (x->flags & HEDDLE_FORCE_BATCHED)) return true;   // weights: batched kernel only
+  if (x->flags & HEDDLE_FORCE_BATCHED) return true;
+  if (wt) return !(x->flags & HEDDLE_FORCE_LAYERED) && k2_smem(x->dtype, x->semiring, n, m, kv, wt) <= x->k2_smem_max;
   if (x->flags & HEDDLE_FORCE_LAYERED) return false;
   return k2_smem(x->dtype, x->semiring, n, m, kv, wt) <= x->k2_smem_max && !use_layered(x, n, m, B);
 }
@@ -488,17 +489,22 @@ heddle_status solve_layered(heddle_place_ctx* x, SolveArgs& a, bool kp, bool kv,
   HP_DISPATCH(fill_launch, a, cells, fill_grid, s);
   pro_for(dt, sr, kp, kv)<<<B, 256, 0, s>>>(a);
   x->launches += 2;
+  const bool wt = a.w != nullptr;
+  if (wt) {   // aggregation weights (R5): prefix sums for the group sizes; the per-layer kernel
+    k8l_weights<<<(B + 127) / 128, 128, 0, s>>>(a);
+    x->launches++;
+  }
   const char* nok5 = std::getenv("HEDDLE_PLACE_NO_PERSISTENT");
-  if (!kp && !kv && !(x->split_world > 1 && (x->split_emulate || !x->p2p)) && !(nok5 && nok5[0] == '1'))
+  if (!kp && !kv && !wt && !(x->split_world > 1 && (x->split_emulate || !x->p2p)) && !(nok5 && nok5[0] == '1'))
     return solve_persistent(x, a, s);
   // tile geometry: 256 columns x kc splits; kc sized for >= ~4 tiles per resident CTA
   // (per rank in split mode: each rank computes 1/world of the layer's cells)
   const double layer_cells = (double)B * (double)(n - m + 1) * (double)(n - m + 2) / 2.0 / x->split_world;
-  K3Fn fn = k3_for(dt, sr, kp, kv);
+  K3Fn fn = k3_for(dt, sr, kp, kv, wt);
   int kc = 2048;
   int occ = 0;
   for (;;) {
-    const int sm = k3_smem(dt, sr, kc);
+    const int sm = k3_smem(dt, sr, kc, wt);
     cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kK3Threads, sm);
     const double tiles = layer_cells / ((double)kK3Cols * kc);
@@ -506,7 +512,7 @@ heddle_status solve_layered(heddle_place_ctx* x, SolveArgs& a, bool kp, bool kv,
     kc /= 2;
   }
   if (occ < 1) return HEDDLE_E_CUDA;
-  const int smem = k3_smem(dt, sr, kc);
+  const int smem = k3_smem(dt, sr, kc, wt);
   LayerArgs la{};
   la.a = a;
   la.kc = kc;
@@ -931,7 +937,7 @@ static heddle_status solve_impl(heddle_place_ctx* x, const heddle_place_problem*
   const bool layered = !ragged && !per_problem_kernel(x, p->n, p->m, p->B, kv, wt);
   if (!layered && !fits) return HEDDLE_E_INVALID;   // n too large for the one-CTA-per-problem kernel
   if (layered && kp && wide && !valley) return HEDDLE_E_INVALID;   // packed (value, split) atomics: 32-bit values
-  if (x->split_world > 1 && (!layered || kp)) return HEDDLE_E_INVALID;  // split mode: layered, no parent table
+  if (x->split_world > 1 && (!layered || kp || wt)) return HEDDLE_E_INVALID;  // split mode: layered, no parent table, no weights
   DeviceGuard guard(x->device);
   SolveArgs a{};
   a.n = p->n;

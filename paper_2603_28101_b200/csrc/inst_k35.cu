@@ -7,7 +7,11 @@
 using namespace hp;
 
 template <int DT, int SR>
-K3Fn pick_k3(bool kp, bool kv) {
+K3Fn pick_k3(bool kp, bool kv, bool w) {
+  if (w) {
+    if (kp) return kv ? k3_layer<DT, SR, true, true, true> : k3_layer<DT, SR, true, false, true>;
+    return kv ? k3_layer<DT, SR, false, true, true> : k3_layer<DT, SR, false, false, true>;
+  }
   if (kp) return kv ? k3_layer<DT, SR, true, true> : k3_layer<DT, SR, true, false>;
   return kv ? k3_layer<DT, SR, false, true> : k3_layer<DT, SR, false, false>;
 }
@@ -16,7 +20,7 @@ KPro pick_pro(bool kp, bool kv) {
   if (kp) return kv ? k3_prologue<DT, SR, true, true> : k3_prologue<DT, SR, true, false>;
   return kv ? k3_prologue<DT, SR, false, true> : k3_prologue<DT, SR, false, false>;
 }
-K3Fn k3_for(int dt, int sr, bool kp, bool kv) { return HP_DISPATCH(pick_k3, kp, kv); }
+K3Fn k3_for(int dt, int sr, bool kp, bool kv, bool w) { return HP_DISPATCH(pick_k3, kp, kv, w); }
 KPro pro_for(int dt, int sr, bool kp, bool kv) { return HP_DISPATCH(pick_pro, kp, kv); }
 template <int DT, int SR>
 K5Fn pick_k5() { return k5_persistent<DT, SR>; }

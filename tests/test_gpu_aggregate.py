@@ -100,3 +100,34 @@ def test_weighted_layered_valley_matches_oracle(n, m, kernel):
     assert int(stt.cpu()[0]) == 0 and float(obj.cpu()[0]) == ref["opt"]
     assert np.array_equal(bnd.cpu().numpy()[0], ref["bounds"])
     pl.close()
+
+
+@pytest.mark.parametrize("keep_parents", [False, True])
+def test_weighted_layered_scan_matches_oracle(keep_parents):
+    """Weights on the per-layer scan kernel (K3, cost gathered per cell): random tiny weighted
+    problems (ties, caps, kv caps, mixed degrees) and a device-aggregated n = 2000 problem, forced
+    onto the layered path; bit-exact against the weighted oracle, back-pointers included."""
+    from tests.parity import assert_exact
+    done = 0
+    for s in range(120):
+        batch = wl.tiny_random(s, n_max=20, m_max=6, allow_caps=True, allow_kv=True, allow_weights=True,
+                               dtype="f32")
+        if batch.weights is None:
+            continue
+        gpu = run_gpu(batch, keep_parents=keep_parents, kernel="layered")
+        ref = oracle.solve(oracle.Problem.from_batch(batch, 0, mode="f32"), want_tables=True)
+        assert_exact(gpu, 0, ref, batch, "f32", "minmax", check_parents=keep_parents, tag=f"w-layered-{s}")
+        gpu["placer"].close()
+        done += 1
+    assert done > 30
+    prof = wl.float_profile()
+    rng = np.random.default_rng(41)
+    n, m = 2000, 12
+    L = wl.presort(wl.predicted(rng, wl.coding_lengths(rng, n // 8, 8)))
+    agg, w, st, na = agg_mod.aggregate(to_dev(L[None, :]), float(np.percentile(L, 60)), 4)
+    k = int(na.cpu()[0])
+    deg = wl.sorted_degree_vectors(rng, 1, m).astype(np.int32)
+    b = wl.Batch("agg2000", k, m, agg[:, :k].cpu().numpy(), deg, prof, weights=w[:, :k].cpu().numpy())
+    gpu = run_gpu(b, keep_parents=keep_parents, kernel="layered")
+    ref = oracle.solve(oracle.Problem.from_batch(b, 0, mode="f32"), want_tables=True, threads=8)
+    assert_exact(gpu, 0, ref, b, "f32", "minmax", check_parents=keep_parents, tag="w-layered-2000")
