@@ -141,6 +141,19 @@ __global__ void __launch_bounds__(256) k3_prologue(SolveArgs a) {
     if (a.rowcap)   // per-worker profile row and cap for K5's tiles (one load instead of three)
       a.rowcap[(int64_t)b * m + j] = make_int2(row < 0 ? 0 : row, a.caps ? a.caps[(int64_t)b * a.cs + j] : -1);
   }
+  int32_t* gWp = a.w ? a.wpws + (int64_t)b * (n + 1) : nullptr;
+  if (a.w && tid == 0) {   // weight prefix sums Wp (R5): exact, left to right; sizes must fit the table
+    int acc = 0;
+    bool ok = true;
+    gWp[0] = 0;
+    for (int t = 0; t < n; ++t) {
+      const int wt = a.w[(int64_t)b * a.ws + t];
+      ok = ok && wt >= 1 && acc <= a.gstride - 1 - wt;
+      acc += wt > 0 ? wt : 0;
+      gWp[t + 1] = acc;
+    }
+    if (!ok) atomicMin(&s_err, (int)HEDDLE_E_RANGE);
+  }
   __syncthreads();
   int err = s_err == INT_MAX ? 0 : s_err;
   if (err == 0 && n < m) err = HEDDLE_E_INFEASIBLE;
@@ -169,7 +182,8 @@ __global__ void __launch_bounds__(256) k3_prologue(SolveArgs a) {
   D* gdp = reinterpret_cast<D*>(a.dpws) + (int64_t)b * (m + 1) * (n + 1);
   const L l0 = gL[0];
   for (int i = 1 + tid; i <= n - m + 1; i += blockDim.x) {
-    D v = T::comb(T::zero(), l0, (cap >= 0 && i > cap) ? T::gpad() : grow[i]);
+    const int sz = gWp ? gWp[i] : i;   // group size of items [0, i)
+    D v = T::comb(T::zero(), l0, (cap >= 0 && sz > cap) ? T::gpad() : grow[sz]);
     if constexpr (KV) { if (kvc >= 0 && gSp[i] - gSp[0] > (S)kvc) v = T::inf(); }
     v = T::norm(v);
     gdp[(int64_t)(n + 1) + i] = v;

@@ -253,7 +253,6 @@ bool per_problem_kernel(const heddle_place_ctx* x, int n, int m, int B, bool kv,
   if (x->flags & HEDDLE_VALLEY)   // K8 whenever the problem fits shared memory, else K8L
     return !(x->flags & HEDDLE_FORCE_LAYERED) && k8_smem(x->dtype, n, m, kv, wt) <= x->k8_smem_max;
   if (x->flags & HEDDLE_FORCE_BATCHED) return true;
-  if (wt) return !(x->flags & HEDDLE_FORCE_LAYERED) && k2_smem(x->dtype, x->semiring, n, m, kv, wt) <= x->k2_smem_max;
   if (x->flags & HEDDLE_FORCE_LAYERED) return false;
   return k2_smem(x->dtype, x->semiring, n, m, kv, wt) <= x->k2_smem_max && !use_layered(x, n, m, B);
 }
@@ -489,11 +488,7 @@ heddle_status solve_layered(heddle_place_ctx* x, SolveArgs& a, bool kp, bool kv,
   HP_DISPATCH(fill_launch, a, cells, fill_grid, s);
   pro_for(dt, sr, kp, kv)<<<B, 256, 0, s>>>(a);
   x->launches += 2;
-  const bool wt = a.w != nullptr;
-  if (wt) {   // aggregation weights (R5): prefix sums for the group sizes; the per-layer kernel
-    k8l_weights<<<(B + 127) / 128, 128, 0, s>>>(a);
-    x->launches++;
-  }
+  const bool wt = a.w != nullptr;   // aggregation weights (R5): the prologue wrote Wp; K3 only
   const char* nok5 = std::getenv("HEDDLE_PLACE_NO_PERSISTENT");
   if (!kp && !kv && !wt && !(x->split_world > 1 && (x->split_emulate || !x->p2p)) && !(nok5 && nok5[0] == '1'))
     return solve_persistent(x, a, s);
@@ -886,12 +881,8 @@ heddle_status solve_valley_layered(heddle_place_ctx* x, SolveArgs& a, bool kp, b
     }
     x->vws = ValleyWs{static_cast<uint32_t*>(mk), bm, sp, smd, static_cast<int*>(dl), nbm, lvm};
   }
-  pro_for(dt, sr, kp, kv)<<<B, 256, 0, s>>>(a);
+  pro_for(dt, sr, kp, kv)<<<B, 256, 0, s>>>(a);   // (also the weight prefix sums, R5)
   x->launches++;
-  if (a.w) {   // aggregation weights (R5): prefix sums for the group sizes
-    k8l_weights<<<(B + 127) / 128, 128, 0, s>>>(a);
-    x->launches++;
-  }
   K8LFn fn = k8l_for(dt, kp, kv, a.w != nullptr);
   for (int j = 1; j <= m; ++j) {
     const int ilo = (j == 1) ? 1 : (j == m ? n : j), ihi = (j == 1 || j < m) ? n - m + j : n;

@@ -516,29 +516,6 @@ __global__ void __launch_bounds__(32 * kK8LWarps, 4) k8l_layer(SolveArgs a, int 
   }
 }
 
-#ifndef HEDDLE_INST_TU   // non-template kernels: defined in heddle_place.cu's translation unit only
-// Weight prefix sums Wp[b][0..n] of aggregated items (R5) for the layered valley solve, after the
-// layered prologue: exact, left to right, one thread per problem; a weight < 1 or a total beyond
-// the cost table makes the problem's status HEDDLE_E_RANGE (as in the one-CTA kernels).
-__global__ void k8l_weights(SolveArgs a) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= a.B || a.status[b] != HEDDLE_OK) return;
-  int32_t* wp = a.wpws + (int64_t)b * (a.n + 1);
-  int acc = 0;
-  bool ok = true;
-  wp[0] = 0;
-  for (int t = 0; t < a.n; ++t) {
-    const int wt = a.w[(int64_t)b * a.ws + t];
-    ok = ok && wt >= 1 && acc <= a.gstride - 1 - wt;
-    acc += wt > 0 ? wt : 0;
-    wp[t + 1] = acc;
-  }
-  if (!ok) {
-    a.status[b] = HEDDLE_E_RANGE;
-    if (a.status_out) a.status_out[b] = HEDDLE_E_RANGE;
-  }
-}
-#endif
 
 // Row j's range-minimum extras, after k8l_layer(j) (one CTA per problem): its last descent, the
 // suffix minima of the descent prefix, and sparse levels >= 1 over the prefix's block minima.

@@ -107,7 +107,7 @@ def test_weighted_layered_scan_matches_oracle(keep_parents):
     """Weights on the per-layer scan kernel (K3, cost gathered per cell): random tiny weighted
     problems (ties, caps, kv caps, mixed degrees) and a device-aggregated n = 2000 problem, forced
     onto the layered path; bit-exact against the weighted oracle, back-pointers included."""
-    from tests.parity import assert_exact
+    from tests.parity import assert_exact, run_gpu
     done = 0
     for s in range(120):
         batch = wl.tiny_random(s, n_max=20, m_max=6, allow_caps=True, allow_kv=True, allow_weights=True,
