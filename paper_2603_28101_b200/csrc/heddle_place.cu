@@ -838,7 +838,7 @@ heddle_status heddle_place_init(const heddle_place_config* c, heddle_place_ctx**
     }
   if (c->flags & HEDDLE_VALLEY) {
     x->k8_smem_max = x->smem_optin;
-    for (int v = 0; v < 16; ++v) {
+    for (int v = 0; v < 24; ++v) {
       const void* fn = reinterpret_cast<const void*>(k8_for(x->dtype, v & 1, (v >> 1) & 1, (v >> 2) & 1, v >> 3));
       cudaFuncAttributes fa{};
       if (cudaFuncGetAttributes(&fa, fn) != cudaSuccess ||
@@ -977,6 +977,12 @@ static heddle_status solve_impl(heddle_place_ctx* x, const heddle_place_problem*
       int wide_min_n = 0;
       if (const char* e = std::getenv("HEDDLE_PLACE_K8_WIDE_MIN_N")) wide_min_n = std::atoi(e);   // tuning
       const bool wide_cta = p->B < x->num_sms && p->n >= wide_min_n;
+      // at most 512 states per layer: 512 threads (one state each, as with 1024, without the idle
+      // warps' instructions)
+      int mid_max_n = 512 + 64;
+      if (const char* e = std::getenv("HEDDLE_PLACE_K8_MID_MAX_N")) mid_max_n = std::atoi(e);   // tuning
+      const int variant = wide_cta ? (p->n - p->m + 1 <= 512 && p->n <= mid_max_n ? 2 : 1) : 0;
+      const int nthreads = variant == 2 ? kK8ThreadsMid : variant == 1 ? kK8ThreadsWide : kK8Threads;
       // few small problems: keep every dp row in shared memory and backtrack inside the kernel
       // (the latency of the rollout-sized call; heddle_place_backtrack then only copies)
       const size_t tab = dp_elem_size(x->dtype, x->semiring) * (size_t)(p->m + 1) * (p->n + 1);
@@ -991,7 +997,7 @@ static heddle_status solve_impl(heddle_place_ctx* x, const heddle_place_problem*
         a.fbounds = x->d_fbounds;
         smem_launch = smem2 + (int)tab;
       }
-      k8_for(x->dtype, kp, kv, wt, wide_cta)<<<p->B, wide_cta ? kK8ThreadsWide : kK8Threads, smem_launch, s>>>(a);
+      k8_for(x->dtype, kp, kv, wt, variant)<<<p->B, nthreads, smem_launch, s>>>(a);
       x->launches++;
       if (cudaGetLastError() != cudaSuccess) return HEDDLE_E_CUDA;
     }

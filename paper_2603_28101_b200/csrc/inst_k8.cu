@@ -16,10 +16,11 @@ K8Fn pick_k8n(bool kp, bool kv, bool w) {
   return kv ? k8_valley<DT, false, true, false, NT> : k8_valley<DT, false, false, false, NT>;
 }
 template <int DT>
-K8Fn pick_k8(bool kp, bool kv, bool w, bool wide) {
-  return wide ? pick_k8n<DT, kK8ThreadsWide>(kp, kv, w) : pick_k8n<DT, kK8Threads>(kp, kv, w);
+K8Fn pick_k8(bool kp, bool kv, bool w, int wide) {
+  return wide == 2 ? pick_k8n<DT, kK8ThreadsMid>(kp, kv, w)
+                   : wide ? pick_k8n<DT, kK8ThreadsWide>(kp, kv, w) : pick_k8n<DT, kK8Threads>(kp, kv, w);
 }
-K8Fn k8_for(int dt, bool kp, bool kv, bool w, bool wide) {
+K8Fn k8_for(int dt, bool kp, bool kv, bool w, int wide) {
   if (dt == HEDDLE_F32) return pick_k8<HEDDLE_F32>(kp, kv, w, wide);
   if (dt == HEDDLE_F64) return pick_k8<HEDDLE_F64>(kp, kv, w, wide);
   return pick_k8<HEDDLE_U32>(kp, kv, w, wide);

@@ -41,6 +41,7 @@ namespace hp {
 // plentiful; 1024 threads when there are fewer problems than SMs (TP sweeps, single instances)
 constexpr int kK8Threads = 128;
 constexpr int kK8ThreadsWide = 1024;
+constexpr int kK8ThreadsMid = 512;   // few problems of at most ~512 states per layer: no idle warps
 constexpr int kVBlk = 32;        // range-minimum block (one 32-bit mask per element)
 constexpr int kScanPrefix = 96;  // default SolveArgs::vscan: descent prefixes shorter than this are
                                  // scanned state by state (no masks / sparse table built)
