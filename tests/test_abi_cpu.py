@@ -117,3 +117,55 @@ def test_split_block_ownership(C):
                 assert max(work) == min(work), (ncb, world, work)
     with pytest.raises(ValueError):
         C.split_blocks(4, 2, 2)
+
+
+def test_round2_entry_points_reject_bad_arguments_without_a_gpu(C):
+    """The round-2 entry points validate their host-side arguments before touching the device:
+    null pointers / sizes / contexts give HEDDLE_E_INVALID (1) and never abort."""
+    L = C.lib()
+    vp = ctypes.c_void_p
+    E_INVALID = 1
+    # state query without a context or with a negative count
+    assert L.heddle_place_query(None, 1, None, None, None, None, None, None) == E_INVALID
+    # aggregation: null buffers, bad sizes / bucket, NaN threshold, unknown dtype
+    buf = (ctypes.c_int32 * 64)()
+    p = ctypes.cast(buf, vp)
+    assert L.heddle_place_aggregate(1, None, 0, 8, 1, 1.0, 2, p, p, p, p, None) == E_INVALID
+    assert L.heddle_place_aggregate(1, p, 0, 0, 1, 1.0, 2, p, p, p, p, None) == E_INVALID
+    assert L.heddle_place_aggregate(1, p, 0, 8, 1, 1.0, 0, p, p, p, p, None) == E_INVALID
+    assert L.heddle_place_aggregate(1, p, 0, 8, 1, float("nan"), 2, p, p, p, p, None) == E_INVALID
+    assert L.heddle_place_aggregate(7, p, 0, 8, 1, 1.0, 2, p, p, p, p, None) == E_INVALID
+    assert L.heddle_place_aggregate(1, p, -1, 8, 1, 1.0, 2, p, p, p, p, None) == E_INVALID
+    # expansion: null buffers, m < 1
+    assert L.heddle_place_expand(None, 2, 1, p, 8, p, None) == E_INVALID
+    assert L.heddle_place_expand(p, 0, 1, p, 8, p, None) == E_INVALID
+    # annealer: null context / arguments
+    args, out = C.AnnealArgs(), C.AnnealOut()
+    assert L.heddle_place_anneal(None, ctypes.byref(args), ctypes.byref(out), None) == E_INVALID
+    # split plan: bad arguments
+    a, b = ctypes.c_int64(0), ctypes.c_int64(0)
+    assert L.heddle_place_split_plan(8, 16, 2, 0, ctypes.byref(a), ctypes.byref(b)) == -1   # n < m
+    assert L.heddle_place_split_plan(16, 8, 2, 2, ctypes.byref(a), ctypes.byref(b)) == -1   # rank >= world
+    assert L.heddle_place_split_plan(16, 8, 2, 0, None, ctypes.byref(b)) == -1
+
+
+def test_problem_struct_layout_matches_header(C):
+    """The ctypes mirrors of the ABI structs carry every field the header declares, in order."""
+    src = open(HEADER).read()
+    def fields_of(body):
+        out = []
+        for names in re.findall(r"^\s*(?:const\s+)?[a-z0-9_]+\*?\s+\*?\s*([A-Za-z_]+(?:\s*,\s*[A-Za-z_]+)*);",
+                                body, re.M):
+            out += [x.strip() for x in names.split(",")]
+        return out
+    body = src[src.index("typedef struct {\n  int32_t n;                    /* trajectories per problem"):]
+    body = body[:body.index("} heddle_place_problem;")]
+    fields = fields_of(body)
+    assert [f[0] for f in C.Problem._fields_] == fields, (fields, C.Problem._fields_)
+    body = src[src.index("} heddle_place_anneal_args;") - 1600:src.index("} heddle_place_anneal_args;")]
+    body = body[body.index("typedef struct {"):]
+    fields = fields_of(body)
+    assert [f[0] for f in C.AnnealArgs._fields_] == fields, (fields, C.AnnealArgs._fields_)
+    body = src[src.index("} heddle_place_anneal_out;") - 1200:src.index("} heddle_place_anneal_out;")]
+    body = body[body.index("typedef struct {"):]
+    assert [f[0] for f in C.AnnealOut._fields_] == fields_of(body)
