@@ -400,6 +400,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k8_valley(SolveArgs a) {
       for (int q = tid; q <= m; q += NT) out[q] = -1;
       return;
     }
+    __syncthreads();   // the last row of the table (its store loop above) is complete
     __shared__ int s_found;
     // the cost rows come from sG, restaged unmasked when the profile row changes (degrees only grow
     // walking back): the lower bound already excludes the groups over a cap.  Without caps the
