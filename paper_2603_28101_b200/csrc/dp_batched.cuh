@@ -22,8 +22,9 @@
 //  * the value pass keeps no argmin (the backtrack kernel recomputes the
 //    lowest-index argmin of the m states it needs); HEDDLE_KEEP_PARENTS
 //    switches to an inner loop with a strict-'<' argmin per transition;
-//  * column blocks are handed out longest-first (LPT) through a shared counter,
-//    and several CTAs share an SM so one CTA's layer barrier is covered by the others.
+//  * column blocks are sorted longest-first (LPT) and dealt to the warps in a static
+//    snake order (HEDDLE_K2_STATIC; 0 = a shared-counter dequeue), and several CTAs
+//    share an SM so one CTA's layer barrier is covered by the others.
 #pragma once
 #include <climits>
 #include <cstdint>
@@ -42,6 +43,9 @@ constexpr int kWarpCols = kColLanes * kLaneCols;   // 64 columns per warp task
 constexpr int kGPad = 131;                   // G padding below s = 0; == 3 (mod 4) for LDS.128 alignment
 constexpr int kGTail = kWarpCols + 8;        // G padding above s = n
 constexpr int kLPad = 4 * kSplitLanes + 24;  // L / dp row padding above n (quarter rounding)
+#ifndef HEDDLE_K2_STATIC
+#define HEDDLE_K2_STATIC 1
+#endif
 #ifndef HEDDLE_K2_WARPS
 #define HEDDLE_K2_WARPS 4
 #endif
@@ -621,11 +625,18 @@ __global__ void __launch_bounds__(kK2Threads, (SR == HEDDLE_MINMAX && DT != HEDD
       const int nblk = (ctop + kWarpCols - 1 - j) / kWarpCols + 1;
       const int kstart = (j - 1) & ~3;
       const int cl = lane & (kColLanes - 1), kg = lane / kColLanes;
+#if HEDDLE_K2_STATIC
+      for (int rnd = 0;; ++rnd) {   // static snake order over the LPT-sorted blocks: no dequeue trip
+        const int t = rnd * kK2Warps + ((rnd & 1) ? kK2Warps - 1 - warp : warp);
+        if (rnd * kK2Warps >= nblk) break;
+        if (t >= nblk) continue;
+#else
       for (;;) {
         int t = 0;
         if (lane == 0) t = atomicAdd(&s_ctr, 1);
         t = __shfl_sync(0xffffffffu, t, 0);
         if (t >= nblk) break;
+#endif
         const int cb = ctop - kWarpCols * t;                  // longest block first (LPT)
         const int c = cb + kLaneCols * cl;
         const int imax = min(cb + kWarpCols - 1, imax_layer);
