@@ -43,6 +43,10 @@ constexpr int kWarpCols = kColLanes * kLaneCols;   // 64 columns per warp task
 constexpr int kGPad = 131;                   // G padding below s = 0; == 3 (mod 4) for LDS.128 alignment
 constexpr int kGTail = kWarpCols + 8;        // G padding above s = n
 constexpr int kLPad = 4 * kSplitLanes + 24;  // L / dp row padding above n (quarter rounding)
+#ifndef HEDDLE_K2_UNROLL
+#define HEDDLE_K2_UNROLL 4
+#endif
+constexpr int kK2Unroll = HEDDLE_K2_UNROLL;   // F32 min-max sweep steps per loop iteration
 #ifndef HEDDLE_K2_STATIC
 #define HEDDLE_K2_STATIC 1
 #endif
@@ -219,7 +223,7 @@ __device__ __forceinline__ void sweep_slide(const typename Tr<DT, SR>::L* __rest
       ld2x2(gk + 2 * q, *reinterpret_cast<unsigned long long(*)[2]>(&wp[q]));
       ld2x2(gk2 + 2 * q, *reinterpret_cast<unsigned long long(*)[2]>(&vp[q]));
     }
-#pragma unroll 4
+#pragma unroll kK2Unroll
     for (int t = 0; t < iters; ++t) {
       float dpv[4], lv[4];
       ld4(sdp + k, dpv);
