@@ -19,7 +19,6 @@ using K5Fn = void (*)(hp::PersistArgs);
 using KPro = void (*)(hp::SolveArgs);
 using K8Fn = void (*)(hp::SolveArgs);
 using K8LFn = void (*)(hp::SolveArgs, int, hp::ValleyWs);
-using K8SFn = void (*)(hp::SolveArgs, int, hp::ValleyWs);
 
 // dt: heddle_dtype, sr: heddle_semiring
 // (HEDDLE_F32X exists only with MINPLUS; heddle_place_init rejects the other combination)
@@ -41,4 +40,3 @@ KPro pro_for(int dt, int sr, bool kp, bool kv);
 K5Fn k5_for(int dt, int sr);
 K8Fn k8_for(int dt, bool kp, bool kv, bool w, int wide);          // inst_k8.cu (0: 128, 1: 1024, 2: 512 threads)
 K8LFn k8l_for(int dt, bool kp, bool kv, bool w = false);
-K8SFn k8lr_for(int dt);

@@ -45,17 +45,6 @@ struct LayerArgs {
   int* err;                      // set on a spin timeout (never hang the device)
 };
 
-// L2 load (bypasses L1: values were produced by other CTAs' atomics)
-template <class D>
-__device__ __forceinline__ D ld_cg(const D* p) {
-  if constexpr (sizeof(D) == 4) {
-    const unsigned v = __ldcg(reinterpret_cast<const unsigned*>(p));
-    return *reinterpret_cast<const D*>(&v);
-  } else {
-    const unsigned long long v = __ldcg(reinterpret_cast<const unsigned long long*>(p));
-    return *reinterpret_cast<const D*>(&v);
-  }
-}
 
 // Spin until *flag >= target (acquire), with a ~10 s timeout that raises *err.
 __device__ __forceinline__ bool wait_flag(const unsigned long long* flag, unsigned long long target, int* err) {
@@ -111,8 +100,9 @@ __global__ void k3_fill(SolveArgs a, int64_t cells) {
 }
 
 // ---------------------------------------------------------------- prologue: validate, Sp, layer 1
+constexpr int kProThreads = 1024;
 template <int DT, int SR, bool KP, bool KV>
-__global__ void __launch_bounds__(256) k3_prologue(SolveArgs a) {
+__global__ void __launch_bounds__(kProThreads) k3_prologue(SolveArgs a) {
   using T = Tr<DT, SR>;
   using L = typename T::L;
   using G = typename T::G;
@@ -123,13 +113,27 @@ __global__ void __launch_bounds__(256) k3_prologue(SolveArgs a) {
   const L* gL = reinterpret_cast<const L*>(a.lengths) + (int64_t)b * a.ls;
   if (tid == 0) s_err = INT_MAX;
   __syncthreads();
-  for (int t = tid; t < n; t += blockDim.x) {
-    const L x = gL[t];
-    bool bad_range;
-    if constexpr (DT == HEDDLE_U32) bad_range = (x == 0u) || (x > a.lmax_u32);
-    else bad_range = !(x > (L)0) || !(x < (L)INFINITY);
-    if (bad_range) atomicMin(&s_err, (int)HEDDLE_E_RANGE);
-    else if (t + 1 < n && gL[t + 1] > x) atomicMin(&s_err, (int)HEDDLE_E_UNSORTED);
+  // U independent pairs of loads in flight per thread (one CTA per problem: a plain strided loop
+  // would wait one memory round trip per element pair)
+  constexpr int U = 8;
+  for (int base = tid; base < n; base += U * kProThreads) {
+    L x[U], y[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int t = min(base + u * kProThreads, n - 1);
+      x[u] = gL[t];
+      y[u] = gL[min(t + 1, n - 1)];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int t = base + u * kProThreads;
+      if (t >= n) continue;
+      bool bad_range;
+      if constexpr (DT == HEDDLE_U32) bad_range = (x[u] == 0u) || (x[u] > a.lmax_u32);
+      else bad_range = !(x[u] > (L)0) || !(x[u] < (L)INFINITY);
+      if (bad_range) atomicMin(&s_err, (int)HEDDLE_E_RANGE);
+      else if (t + 1 < n && y[u] > x[u]) atomicMin(&s_err, (int)HEDDLE_E_UNSORTED);
+    }
   }
   int row1 = 0;
   for (int j = tid; j < m; j += blockDim.x) {
@@ -181,13 +185,27 @@ __global__ void __launch_bounds__(256) k3_prologue(SolveArgs a) {
   const int64_t kvc = KV ? a.kv[(int64_t)b * a.kvs] : -1;
   D* gdp = reinterpret_cast<D*>(a.dpws) + (int64_t)b * (m + 1) * (n + 1);
   const L l0 = gL[0];
-  for (int i = 1 + tid; i <= n - m + 1; i += blockDim.x) {
-    const int sz = gWp ? gWp[i] : i;   // group size of items [0, i)
-    D v = T::comb(T::zero(), l0, (cap >= 0 && sz > cap) ? T::gpad() : grow[sz]);
-    if constexpr (KV) { if (kvc >= 0 && gSp[i] - gSp[0] > (S)kvc) v = T::inf(); }
-    v = T::norm(v);
-    gdp[(int64_t)(n + 1) + i] = v;
-    if (KP) a.parws[(int64_t)b * (m + 1) * (n + 1) + (n + 1) + i] = (v == T::inf()) ? -1 : 0;
+  const int i1 = n - m + 1;
+  for (int base = 1 + tid; base <= i1; base += U * kProThreads) {
+    int sz[U];
+    G g[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = min(base + u * kProThreads, i1);
+      sz[u] = gWp ? gWp[i] : i;   // group size of items [0, i)
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) g[u] = (cap >= 0 && sz[u] > cap) ? T::gpad() : grow[sz[u]];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + u * kProThreads;
+      if (i > i1) continue;
+      D v = T::comb(T::zero(), l0, g[u]);
+      if constexpr (KV) { if (kvc >= 0 && gSp[i] - gSp[0] > (S)kvc) v = T::inf(); }
+      v = T::norm(v);
+      gdp[(int64_t)(n + 1) + i] = v;
+      if (KP) a.parws[(int64_t)b * (m + 1) * (n + 1) + (n + 1) + i] = (v == T::inf()) ? -1 : 0;
+    }
   }
 }
 

@@ -486,7 +486,7 @@ heddle_status solve_layered(heddle_place_ctx* x, SolveArgs& a, bool kp, bool kv,
   const int64_t cells = (int64_t)B * (m + 1) * (n + 1);
   const int fill_grid = (int)std::min<int64_t>((cells + 255) / 256, (int64_t)x->num_sms * 16);
   HP_DISPATCH(fill_launch, a, cells, fill_grid, s);
-  pro_for(dt, sr, kp, kv)<<<B, 256, 0, s>>>(a);
+  pro_for(dt, sr, kp, kv)<<<B, kProThreads, 0, s>>>(a);
   x->launches += 2;
   const bool wt = a.w != nullptr;   // aggregation weights (R5): the prologue wrote Wp; K3 only
   const char* nok5 = std::getenv("HEDDLE_PLACE_NO_PERSISTENT");
@@ -695,6 +695,8 @@ void heddle_place_destroy(heddle_place_ctx* ctx) {
   cudaFree(ctx->vws.sp);
   cudaFree(ctx->vws.smd);
   cudaFree(ctx->vws.dlast);
+  cudaFree(ctx->vws.dlrun);
+  cudaFree(ctx->vws.done);
   if (ctx->h_epoch) cudaFreeHost(ctx->h_epoch);
   cudaFree(ctx->d_klo);
   cudaFree(ctx->d_wp);
@@ -869,30 +871,46 @@ heddle_status solve_valley_layered(heddle_place_ctx* x, SolveArgs& a, bool kp, b
     const int nbm = vblocks(x->max_n), lvm = vlevels(nbm);
     const size_t des = dp_elem_size(x->dtype, x->semiring);
     void* mk = nullptr;
-    void *bm = nullptr, *sp = nullptr, *smd = nullptr, *dl = nullptr;
+    void *bm = nullptr, *sp = nullptr, *smd = nullptr, *dl = nullptr, *dr = nullptr, *dn = nullptr;
     if (cudaMalloc(&mk, 4 * 2 * (size_t)x->max_batch * nbm * kVBlk) != cudaSuccess ||
         cudaMalloc(&bm, des * 2 * (size_t)x->max_batch * nbm) != cudaSuccess ||
         cudaMalloc(&sp, des * (size_t)x->max_batch * std::max(1, lvm - 1) * nbm) != cudaSuccess ||
         cudaMalloc(&smd, des * (size_t)x->max_batch * (x->max_n + 1)) != cudaSuccess ||
-        cudaMalloc(&dl, 4 * (size_t)x->max_batch) != cudaSuccess) {
+        cudaMalloc(&dl, 4 * (size_t)x->max_batch) != cudaSuccess ||
+        cudaMalloc(&dr, 4 * 2 * (size_t)x->max_batch) != cudaSuccess ||
+        cudaMalloc(&dn, 4 * (size_t)x->max_batch) != cudaSuccess) {
       cudaGetLastError();
-      for (void* q : {mk, bm, sp, smd, dl}) cudaFree(q);
+      for (void* q : {mk, bm, sp, smd, dl, dr, dn}) cudaFree(q);
       return HEDDLE_E_NOMEM;
     }
-    x->vws = ValleyWs{static_cast<uint32_t*>(mk), bm, sp, smd, static_cast<int*>(dl), nbm, lvm};
+    x->vws = ValleyWs{static_cast<uint32_t*>(mk), bm, sp, smd, static_cast<int*>(dl), static_cast<int*>(dr),
+                      static_cast<unsigned*>(dn), nbm, lvm};
   }
-  pro_for(dt, sr, kp, kv)<<<B, 256, 0, s>>>(a);   // (also the weight prefix sums, R5)
+  // per solve: no in-run descents yet, no finished CTAs (the last CTA of each layer resets both)
+  if (cudaMemsetAsync(x->vws.dlrun, 0xFF, 4 * 2 * (size_t)B, s) != cudaSuccess ||
+      cudaMemsetAsync(x->vws.done, 0, 4 * (size_t)B, s) != cudaSuccess)
+    return HEDDLE_E_CUDA;
+  pro_for(dt, sr, kp, kv)<<<B, kProThreads, 0, s>>>(a);   // (also the weight prefix sums, R5)
   x->launches++;
   K8LFn fn = k8l_for(dt, kp, kv, a.w != nullptr);
+  // programmatic dependent launch: layer j+1's CTAs are scheduled while layer j runs and wait in
+  // griddepcontrol.wait for its completion (no launch gap on the layer chain)
+  static const bool pdl = !std::getenv("HEDDLE_PLACE_NO_PDL");   // A/B switch
+  cudaLaunchAttribute attr{};
+  attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr.val.programmaticStreamSerializationAllowed = 1;
   for (int j = 1; j <= m; ++j) {
     const int ilo = (j == 1) ? 1 : (j == m ? n : j), ihi = (j == 1 || j < m) ? n - m + j : n;
-    const int warps = ((ihi >> 5) - (ilo >> 5) + 1 + 3) / 4;
-    fn<<<dim3((warps + kK8LWarps - 1) / kK8LWarps, B), 32 * kK8LWarps, 0, s>>>(a, j, x->vws);
+    const int warps = ((ihi >> 5) - (ilo >> 5) + kK8LRun) / kK8LRun;
+    // (row j's range-minimum extras are built by the last CTA of the launch to finish)
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((warps + kK8LWarps - 1) / kK8LWarps, B);
+    cfg.blockDim = dim3(32 * kK8LWarps);
+    cfg.stream = s;
+    cfg.attrs = &attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    if (cudaLaunchKernelEx(&cfg, fn, a, j, x->vws) != cudaSuccess) return HEDDLE_E_CUDA;
     x->launches++;
-    if (j < m) {
-      k8lr_for(dt)<<<B, 1024, 0, s>>>(a, j, x->vws);
-      x->launches++;
-    }
   }
   HP_DISPATCH(finalize_launch, a, s);
   x->launches++;

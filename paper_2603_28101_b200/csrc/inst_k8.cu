@@ -39,8 +39,3 @@ K8LFn k8l_for(int dt, bool kp, bool kv, bool w) {
   if (dt == HEDDLE_F64) return pick_k8l<HEDDLE_F64>(kp, kv, w);
   return pick_k8l<HEDDLE_U32>(kp, kv, w);
 }
-K8SFn k8lr_for(int dt) {
-  if (dt == HEDDLE_F32) return k8l_rowprep<HEDDLE_F32>;
-  if (dt == HEDDLE_F64) return k8l_rowprep<HEDDLE_F64>;
-  return k8l_rowprep<HEDDLE_U32>;
-}

@@ -157,4 +157,16 @@ __device__ __forceinline__ void ld4<uint64_t>(const uint64_t* p, uint64_t (&o)[4
   o[0] = a.x; o[1] = a.y; o[2] = b.x; o[3] = b.y;
 }
 
+// L2 load (bypasses L1: values produced by other CTAs of the same launch)
+template <class D>
+__device__ __forceinline__ D ld_cg(const D* p) {
+  if constexpr (sizeof(D) == 4) {
+    const unsigned v = __ldcg(reinterpret_cast<const unsigned*>(p));
+    return *reinterpret_cast<const D*>(&v);
+  } else {
+    const unsigned long long v = __ldcg(reinterpret_cast<const unsigned long long*>(p));
+    return *reinterpret_cast<const D*>(&v);
+  }
+}
+
 }  // namespace hp

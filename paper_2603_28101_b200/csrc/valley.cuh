@@ -152,7 +152,9 @@ struct Valley {   // ROWPAD: `grow` is the worker's row staged for every size 0.
   // dp[j][i] over splits [lo, i-1]; `from` >= lo is a split before which the crossing cannot
   // lie (the previous state's k*); returns the value, the lowest argmin (if wanted) and k*.
   // MONO: row j-1 has no descent (dlast < 0), so every range minimum is the row's own value
-  template <bool ARG, bool MONO = false>
+  // KARY > 2: wide intervals take KARY - 1 independent probes per step (a chain of log_KARY
+  // dependent loads instead of log_2: for K8L, whose probes are L2 round trips)
+  template <bool ARG, bool MONO = false, int KARY = 2>
   __device__ __forceinline__ D solve(int lo, int i, int from, int& arg, int& kstar) const {
     const int hi = i - 1;
     auto R = [&](int k, int e) -> D {
@@ -179,6 +181,26 @@ struct Valley {   // ROWPAD: `grow` is the worker's row staged for every size 0.
       }
     }                            // else: plain bisection of [lo, hi]
     bool have_rt = t <= hi;
+    if constexpr (KARY > 2) {
+      while (t - f > 2 * KARY) {
+        const int q = (t - f) / KARY;
+        D r[KARY - 1], c[KARY - 1];
+#pragma unroll
+        for (int u = 0; u < KARY - 1; ++u) {
+          r[u] = R(f + (u + 1) * q, hi);
+          c[u] = cost(f + (u + 1) * q, i);
+        }
+        int nf = f, nt = t;
+#pragma unroll
+        for (int u = KARY - 2; u >= 0; --u)   // the lowest crossed probe
+          if (r[u] >= c[u]) { nt = f + (u + 1) * q; rm_t = r[u]; have_rt = true; }
+#pragma unroll
+        for (int u = 0; u < KARY - 1; ++u)    // the highest probe not crossed
+          if (!(r[u] >= c[u])) { nf = f + (u + 1) * q; c_f = c[u]; have_cf = true; }
+        f = nf;
+        t = nt;
+      }
+    }
     while (t - f > 1) {
       const int mid = (f + t) >> 1;
       if (crossed(mid)) { t = mid; have_rt = true; } else { f = mid; have_cf = true; }
@@ -442,8 +464,18 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k8_valley(SolveArgs a) {
 // dp rows live in the workspace (L2-resident per layer).  A warp owns 4 consecutive 32-element
 // blocks of the row (a lane: 4 consecutive states, galloping), then builds their masks and minima
 // for the next layer.  Validation and prefix sums come from the layered prologue.
-constexpr int kK8LRun = 4;
-constexpr int kK8LWarps = 8;
+#ifndef HEDDLE_K8L_RUN
+#define HEDDLE_K8L_RUN 1
+#endif
+#ifndef HEDDLE_K8L_WARPS
+#define HEDDLE_K8L_WARPS 8
+#endif
+constexpr int kK8LRun = HEDDLE_K8L_RUN;      // consecutive states per lane (= 32-element blocks per warp)
+constexpr int kK8LWarps = HEDDLE_K8L_WARPS;
+#ifndef HEDDLE_K8L_KARY
+#define HEDDLE_K8L_KARY 4
+#endif
+constexpr int kK8LKary = HEDDLE_K8L_KARY;    // probes + 1 per step of a state's first crossing search
 
 struct ValleyWs {                // K8L range-minimum workspace (per problem, row parity p = j & 1)
   uint32_t* mask;                // [2][B][nb*32]
@@ -451,8 +483,79 @@ struct ValleyWs {                // K8L range-minimum workspace (per problem, ro
   void* sp;                      // [B][levels-1][nb] sparse levels >= 1 (rebuilt per row)
   void* smd;                     // [B][max_n+1]      suffix minima of the descent prefix (per row)
   int* dlast;                    // [B]               last descent of the row (-1: none)
+  int* dlrun;                    // [2][B]            descents inside the warps' runs (-1; by parity)
+  unsigned* done;                // [B]               CTAs of the current layer finished
   int nbmax, lvmax;
 };
+
+// Row j's range-minimum extras, by the last CTA of layer j to finish (`nt` threads): the last
+// descent of the row (the largest of the in-run descents the warps found and the pairs across
+// 32-element blocks), the suffix minima of the descent prefix, and sparse levels >= 1 over the
+// prefix's block minima.  Reads of row j and of the block minima written by other CTAs of this
+// launch go through L2 (ld.cg).
+template <class T>
+__device__ __forceinline__ void k8l_row_extras(const SolveArgs& a, int j, const ValleyWs& w, int b, int tid, int nt,
+                                               int* s_dl) {
+  using D = typename T::D;
+  const int n = a.n, m = a.m;
+  const int ilo = (j == 1) ? 1 : j, ihi = n - m + j, nb = vblocks(n);
+  const D* row = reinterpret_cast<const D*>(a.dpws) + ((int64_t)b * (m + 1) + j) * (n + 1);
+  int* run_slot = w.dlrun + (int64_t)(j & 1) * a.B + b;
+  int myd = -1;
+  constexpr int U = 8;   // block-boundary pairs (t = 32 q + 31, t + 1), U pairs of loads in flight
+  for (int q0 = (ilo >> 5) + tid; (q0 << 5) + 31 < ihi; q0 += U * nt) {
+    D x[U], y[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int t = min(((q0 + u * nt) << 5) + 31, ihi - 1);
+      x[u] = ld_cg(row + t);
+      y[u] = ld_cg(row + t + 1);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int t = ((q0 + u * nt) << 5) + 31;
+      if (t >= ilo && t < ihi && x[u] > y[u]) myd = max(myd, t);
+    }
+  }
+  myd = __reduce_max_sync(0xffffffffu, myd);
+  if ((tid & 31) == 0 && myd >= 0) atomicMax(s_dl, myd);
+  __syncthreads();
+  const int dl = max(*s_dl, ld_cg(run_slot));
+  __syncthreads();
+  if (tid == 0) {
+    w.dlast[b] = dl;
+    *run_slot = -1;   // the slot of parity j & 1 is next written by layer j + 2
+    w.done[b] = 0;
+  }
+  if (dl < 0) return;
+  if (tid < 32) {   // smd[k] = min(row[k..dl+1]) (suffix scans of 32, right to left)
+    D* smd = reinterpret_cast<D*>(w.smd) + (int64_t)b * (n + 1);
+    D carry = T::inf();
+    for (int base = dl + 1 - 31;; base -= 32) {
+      const int idx = base + tid;
+      D x = (idx >= ilo) ? ld_cg(row + idx) : T::inf();
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const D y = __shfl_down_sync(0xffffffffu, x, off);
+        if (tid + off < 32) x = T::vmin(x, y);
+      }
+      x = T::vmin(x, carry);
+      if (idx >= ilo) smd[idx] = x;
+      carry = __shfl_sync(0xffffffffu, x, 0);
+      if (base <= ilo) break;
+    }
+  }
+  const int blo = ilo >> 5, bhi = dl >> 5;
+  const D* bmj = reinterpret_cast<const D*>(w.bm) + ((int64_t)(j & 1) * a.B + b) * nb;
+  D* sp = reinterpret_cast<D*>(w.sp) + (int64_t)b * (w.lvmax - 1) * nb;
+  for (int l = 1; (1 << l) <= bhi - blo + 1; ++l) {
+    const D* src = l == 1 ? bmj : sp + (int64_t)(l - 2) * nb;
+    D* dst = sp + (int64_t)(l - 1) * nb;
+    for (int blk = blo + tid; blk + (1 << l) - 1 <= bhi; blk += nt)
+      dst[blk] = T::vmin(ld_cg(src + blk), ld_cg(src + blk + (1 << (l - 1))));
+    __syncthreads();
+  }
+}
 
 template <int DT, bool KP, bool KV, bool W = false>
 __global__ void __launch_bounds__(32 * kK8LWarps, 4) k8l_layer(SolveArgs a, int j, ValleyWs w) {
@@ -461,97 +564,93 @@ __global__ void __launch_bounds__(32 * kK8LWarps, 4) k8l_layer(SolveArgs a, int 
   using G = typename T::G;
   using D = typename T::D;
   using S = typename SpT<DT>::type;
-  __shared__ D s_row[kK8LWarps][128];
-  const int n = a.n, m = a.m, b = blockIdx.y, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (a.status[b] != HEDDLE_OK) return;
+  __shared__ D s_row[kK8LWarps][32 * kK8LRun];
+  __shared__ int s_dl, s_last;
+  const int n = a.n, m = a.m, b = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // launched with programmatic stream serialisation: wait until the previous layer's grid has
+  // completed and its stores are visible (the next layer's grid is released after the states)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (a.status[b] != HEDDLE_OK) return;   // (uniform over the problem's CTAs)
   const int ilo = (j == 1) ? 1 : (j == m ? n : j);
   const int ihi = (j == 1 || j < m) ? n - m + j : n;
-  const int blk0 = (ilo >> 5) + 4 * (blockIdx.x * kK8LWarps + warp);
-  if ((blk0 << 5) > ihi) return;
+  const int blk0 = (ilo >> 5) + kK8LRun * (blockIdx.x * kK8LWarps + warp);
+  const bool active = (blk0 << 5) <= ihi;
+  if (tid == 0) s_dl = -1;
   const int nb = vblocks(n);
   D* gdp = reinterpret_cast<D*>(a.dpws) + (int64_t)b * (m + 1) * (n + 1);
-  const int d = a.degrees[(int64_t)b * a.ds + j - 1];
-  int row = 0;
-  for (int q = 0; q < a.D; ++q) row = (a.prof_deg[q] == d) ? q : row;
-  const int cap = a.caps ? a.caps[(int64_t)b * a.cs + j - 1] : -1;
-  const int pp = (j - 1) & 1;
-  const RowMin<T> rm{gdp + (int64_t)(j - 1) * (n + 1), reinterpret_cast<const D*>(w.smd) + (int64_t)b * (n + 1),
-                     w.mask + ((int64_t)pp * a.B + b) * nb * kVBlk,
-                     reinterpret_cast<const D*>(w.bm) + ((int64_t)pp * a.B + b) * nb,
-                     reinterpret_cast<const D*>(w.sp) + (int64_t)b * (w.lvmax - 1) * nb, nb,
-                     j > 1 ? w.dlast[b] : -1};
-  Valley<DT, KV, W> V{reinterpret_cast<const L*>(a.lengths) + (int64_t)b * a.ls, rm,
-                      reinterpret_cast<const G*>(a.gtab) + (int64_t)row * a.gstride,
-                      KV ? reinterpret_cast<const S*>(a.spws) + (int64_t)b * (n + 1) : nullptr,
-                      W ? a.wpws + (int64_t)b * (n + 1) : nullptr,
-                          (cap >= 0 && cap < a.gstride - 1) ? cap : a.gstride - 1,
-                          KV ? a.kv[(int64_t)b * a.kvs + j - 1] : -1, false};
   const int x0 = (blk0 << 5) + kK8LRun * lane;
-  int from = j - 1;
+  if (active) {
+    const int d = a.degrees[(int64_t)b * a.ds + j - 1];
+    int row = 0;
+    for (int q = 0; q < a.D; ++q) row = (a.prof_deg[q] == d) ? q : row;
+    const int cap = a.caps ? a.caps[(int64_t)b * a.cs + j - 1] : -1;
+    const int pp = (j - 1) & 1;
+    const RowMin<T> rm{gdp + (int64_t)(j - 1) * (n + 1), reinterpret_cast<const D*>(w.smd) + (int64_t)b * (n + 1),
+                       w.mask + ((int64_t)pp * a.B + b) * nb * kVBlk,
+                       reinterpret_cast<const D*>(w.bm) + ((int64_t)pp * a.B + b) * nb,
+                       reinterpret_cast<const D*>(w.sp) + (int64_t)b * (w.lvmax - 1) * nb, nb,
+                       j > 1 ? w.dlast[b] : -1};
+    Valley<DT, KV, W> V{reinterpret_cast<const L*>(a.lengths) + (int64_t)b * a.ls, rm,
+                        reinterpret_cast<const G*>(a.gtab) + (int64_t)row * a.gstride,
+                        KV ? reinterpret_cast<const S*>(a.spws) + (int64_t)b * (n + 1) : nullptr,
+                        W ? a.wpws + (int64_t)b * (n + 1) : nullptr,
+                            (cap >= 0 && cap < a.gstride - 1) ? cap : a.gstride - 1,
+                            KV ? a.kv[(int64_t)b * a.kvs + j - 1] : -1, false};
+    int from = j - 1;
 #pragma unroll
-  for (int r = 0; r < kK8LRun; ++r) {
-    const int i = x0 + r;
-    D v = T::inf();
-    if (i >= ilo && i <= ihi) {
-      int arg = -1, ks = from;
-      if (j == 1) {
-        v = V.cost(0, i);
-        arg = (v == T::inf()) ? -1 : 0;
-      } else {
-        v = rm.dlast < 0 ? V.template solve<KP, true>(j - 1, i, from, arg, ks)   // monotone row j-1
-                         : V.template solve<KP>(j - 1, i, from, arg, ks);
-        from = ks;
+    for (int r = 0; r < kK8LRun; ++r) {
+      const int i = x0 + r;
+      D v = T::inf();
+      if (i >= ilo && i <= ihi) {
+        int arg = -1, ks = from;
+        if (j == 1) {
+          v = V.cost(0, i);
+          arg = (v == T::inf()) ? -1 : 0;
+        } else {
+          v = rm.dlast < 0 ? V.template solve<KP, true, kK8LKary>(j - 1, i, from, arg, ks)   // monotone row j-1
+                           : V.template solve<KP, false, kK8LKary>(j - 1, i, from, arg, ks);
+          from = ks;
+        }
+        gdp[(int64_t)j * (n + 1) + i] = v;
+        if (KP) a.parws[((int64_t)b * (m + 1) + j) * (n + 1) + i] = arg;
       }
-      gdp[(int64_t)j * (n + 1) + i] = v;
-      if (KP) a.parws[((int64_t)b * (m + 1) + j) * (n + 1) + i] = arg;
+      s_row[warp][kK8LRun * lane + r] = v;
     }
-    s_row[warp][kK8LRun * lane + r] = v;
   }
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (j == m) return;   // the last row is never queried
   __syncwarp();
-  if (lane < 4 && blk0 + lane <= (ihi >> 5)) {   // masks + minimum of block blk0 + lane of row j
-    const int p = j & 1;
-    uint32_t* mk = w.mask + ((int64_t)p * a.B + b) * nb * kVBlk;
-    D* bmj = reinterpret_cast<D*>(w.bm) + ((int64_t)p * a.B + b) * nb;
-    const int blk = blk0 + lane;
-    block_masks<T>(s_row[warp] + 32 * lane, ilo - (blk << 5), ihi - (blk << 5), mk + (blk << 5), bmj + blk);
-  }
-}
-
-
-// Row j's range-minimum extras, after k8l_layer(j) (one CTA per problem): its last descent, the
-// suffix minima of the descent prefix, and sparse levels >= 1 over the prefix's block minima.
-template <int DT>
-__global__ void __launch_bounds__(1024) k8l_rowprep(SolveArgs a, int j, ValleyWs w) {
-  using T = Tr<DT, HEDDLE_MINMAX>;
-  using D = typename T::D;
-  __shared__ int s_dl;
-  const int n = a.n, m = a.m, b = blockIdx.x, tid = threadIdx.x;
-  if (a.status[b] != HEDDLE_OK) return;
-  const int ilo = (j == 1) ? 1 : j, ihi = n - m + j, nb = vblocks(n);
-  const D* row = reinterpret_cast<const D*>(a.dpws) + ((int64_t)b * (m + 1) + j) * (n + 1);
-  if (tid == 0) s_dl = -1;
-  __syncthreads();
   int myd = -1;
-  for (int t = ilo + tid; t < ihi; t += blockDim.x)
-    if (row[t] > row[t + 1]) myd = t;
-  myd = __reduce_max_sync(0xffffffffu, myd);
-  if ((tid & 31) == 0 && myd >= 0) atomicMax(&s_dl, myd);
-  __syncthreads();
-  const int dl = s_dl;
-  if (tid == 0) w.dlast[b] = dl;
-  if (dl < 0) return;
-  if (tid < 32) suffix_min_warp<T>(row, ilo, dl + 1, reinterpret_cast<D*>(w.smd) + (int64_t)b * (n + 1), tid);
-  const int blo = ilo >> 5, bhi = dl >> 5;
-  const D* bmj = reinterpret_cast<const D*>(w.bm) + ((int64_t)(j & 1) * a.B + b) * nb;
-  D* sp = reinterpret_cast<D*>(w.sp) + (int64_t)b * (w.lvmax - 1) * nb;
-  for (int l = 1; (1 << l) <= bhi - blo + 1; ++l) {
-    const D* src = l == 1 ? bmj : sp + (int64_t)(l - 2) * nb;
-    D* dst = sp + (int64_t)(l - 1) * nb;
-    for (int blk = blo + tid; blk + (1 << l) - 1 <= bhi; blk += blockDim.x)
-      dst[blk] = T::vmin(src[blk], src[blk + (1 << (l - 1))]);
-    __syncthreads();
+  if (active) {
+    if (lane < kK8LRun && blk0 + lane <= (ihi >> 5)) {   // masks + minimum of block blk0 + lane of row j
+      const int p = j & 1;
+      uint32_t* mk = w.mask + ((int64_t)p * a.B + b) * nb * kVBlk;
+      D* bmj = reinterpret_cast<D*>(w.bm) + ((int64_t)p * a.B + b) * nb;
+      const int blk = blk0 + lane;
+      block_masks<T>(s_row[warp] + 32 * lane, ilo - (blk << 5), ihi - (blk << 5), mk + (blk << 5), bmj + blk);
+    }
+    // descents v[t] > v[t+1] inside the warp's run (pairs across warps: the last CTA)
+#pragma unroll
+    for (int r = 0; r < kK8LRun; ++r) {
+      const int q = kK8LRun * lane + r, t = x0 + r;
+      if (q + 1 < 32 * kK8LRun && t >= ilo && t + 1 <= ihi && s_row[warp][q] > s_row[warp][q + 1]) myd = t;
+    }
   }
+  myd = __reduce_max_sync(0xffffffffu, myd);
+  __syncthreads();   // (s_dl initialised)
+  if (lane == 0 && myd >= 0) atomicMax(&s_dl, myd);
+  __threadfence();   // this thread's row / mask / minimum stores before the completion count
+  __syncthreads();
+  if (tid == 0) {
+    if (s_dl >= 0) atomicMax(w.dlrun + (int64_t)(j & 1) * a.B + b, s_dl);
+    __threadfence();
+    s_last = atomicAdd(w.done + b, 1u) == gridDim.x - 1;
+    s_dl = -1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  k8l_row_extras<T>(a, j, w, b, tid, 32 * kK8LWarps, &s_dl);
 }
 
 }  // namespace hp

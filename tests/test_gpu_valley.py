@@ -117,6 +117,21 @@ def test_valley_medium_layered_vs_oracle():
     assert np.array_equal(gpu["bounds"], bounds)
 
 
+def test_valley_layered_batched_mixed_degrees():
+    """K8L (forced layered) on 64 bench problems with mixed degrees -- rows whose descents fall
+    inside a warp's run and across the 32-element blocks of different CTAs, found by the layer's
+    last CTA (row extras fused into the layer launch) -- and on the TP sweep: identical to the
+    oracle's objectives and boundaries."""
+    for batch, shared in ((wl.config_batched(B=64), False), (wl.config_tp_sweep(), True)):
+        gpu = run_gpu(batch, lengths_shared=shared, kernel="layered", algo="valley")
+        rows = np.stack([batch.profile.row_of(batch.degrees[b]) for b in range(batch.B)])
+        opt, bounds, _ = oracle.solve_batch(batch.lengths, batch.profile.T, batch.profile.F, rows, mode="f32",
+                                            threads=4)
+        assert np.all(gpu["status"] == 0)
+        assert np.array_equal(gpu["obj"], opt), batch.name
+        assert np.array_equal(gpu["bounds"], bounds), batch.name
+
+
 def test_valley_full_launches_equal_scan(vscan):
     """The bench launches: all 16384 batched problems and the n = 65536, m = 256 instance --
     valley objectives and boundaries identical to the full scan's, problem by problem, and
