@@ -890,6 +890,10 @@ heddle_status solve_valley_layered(heddle_place_ctx* x, SolveArgs& a, bool kp, b
   if (cudaMemsetAsync(x->vws.dlrun, 0xFF, 4 * 2 * (size_t)B, s) != cudaSuccess ||
       cudaMemsetAsync(x->vws.done, 0, 4 * (size_t)B, s) != cudaSuccess)
     return HEDDLE_E_CUDA;
+  if (!x->d_rowcap) {
+    if (cudaMalloc(&x->d_rowcap, sizeof(int2) * (size_t)x->max_batch * x->max_m) != cudaSuccess) { cudaGetLastError(); return HEDDLE_E_NOMEM; }
+  }
+  a.rowcap = x->d_rowcap;   // {profile row, cap} per worker: one load per layer launch
   pro_for(dt, sr, kp, kv)<<<B, kProThreads, 0, s>>>(a);   // (also the weight prefix sums, R5)
   x->launches++;
   K8LFn fn = k8l_for(dt, kp, kv, a.w != nullptr);

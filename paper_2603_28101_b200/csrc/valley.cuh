@@ -117,6 +117,31 @@ __device__ __forceinline__ void block_masks(const typename T::D* vals, int lo, i
   *bm = val(__ffs(st) - 1);
 }
 
+// The same masks and minimum of one 32-element block by a whole warp, lane t producing mask[t]:
+// bit t, and bit h < t iff vals[h] < min(vals[h+1..t]) (h walks down from 31, vals[h] broadcast),
+// so the warp issues ~32 uniform steps instead of one lane's serial staircase.
+template <class T>
+__device__ __forceinline__ void block_masks_warp(const typename T::D* vals, int lo, int hi, uint32_t* mask,
+                                                 typename T::D* bm, int lane) {
+  using D = typename T::D;
+  const D x = (lane >= lo && lane <= hi) ? vals[lane] : T::inf();
+  uint32_t st = 0;
+  D run = T::inf();
+#pragma unroll
+  for (int h = 31; h >= 0; --h) {
+    const D vh = __shfl_sync(0xffffffffu, x, h);
+    if (h <= lane) {
+      if (h == lane || vh < run) st |= 1u << h;   // (t itself always: also when +inf)
+      run = T::vmin(run, vh);
+    }
+  }
+  mask[lane] = st;
+  D mn = x;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) mn = T::vmin(mn, __shfl_xor_sync(0xffffffffu, mn, off));
+  if (lane == 0) *bm = mn;
+}
+
 // The layer's group cost and the valley search, shared by the shared-memory (K8) and the
 // global-memory (K8L) kernels.  Pointers address one problem; sizes are item counts, or weight
 // sums with aggregation weights (R5).
@@ -558,7 +583,7 @@ __device__ __forceinline__ void k8l_row_extras(const SolveArgs& a, int j, const 
 }
 
 template <int DT, bool KP, bool KV, bool W = false>
-__global__ void __launch_bounds__(32 * kK8LWarps, 4) k8l_layer(SolveArgs a, int j, ValleyWs w) {
+__global__ void __launch_bounds__(32 * kK8LWarps, DT == HEDDLE_F64 ? 2 : 4) k8l_layer(SolveArgs a, int j, ValleyWs w) {
   using T = Tr<DT, HEDDLE_MINMAX>;
   using L = typename T::L;
   using G = typename T::G;
@@ -580,10 +605,8 @@ __global__ void __launch_bounds__(32 * kK8LWarps, 4) k8l_layer(SolveArgs a, int 
   D* gdp = reinterpret_cast<D*>(a.dpws) + (int64_t)b * (m + 1) * (n + 1);
   const int x0 = (blk0 << 5) + kK8LRun * lane;
   if (active) {
-    const int d = a.degrees[(int64_t)b * a.ds + j - 1];
-    int row = 0;
-    for (int q = 0; q < a.D; ++q) row = (a.prof_deg[q] == d) ? q : row;
-    const int cap = a.caps ? a.caps[(int64_t)b * a.cs + j - 1] : -1;
+    const int2 rc = a.rowcap[(int64_t)b * m + j - 1];   // {profile row, cap} from the prologue
+    const int row = rc.x, cap = rc.y;
     const int pp = (j - 1) & 1;
     const RowMin<T> rm{gdp + (int64_t)(j - 1) * (n + 1), reinterpret_cast<const D*>(w.smd) + (int64_t)b * (n + 1),
                        w.mask + ((int64_t)pp * a.B + b) * nb * kVBlk,
@@ -622,12 +645,15 @@ __global__ void __launch_bounds__(32 * kK8LWarps, 4) k8l_layer(SolveArgs a, int 
   __syncwarp();
   int myd = -1;
   if (active) {
-    if (lane < kK8LRun && blk0 + lane <= (ihi >> 5)) {   // masks + minimum of block blk0 + lane of row j
-      const int p = j & 1;
-      uint32_t* mk = w.mask + ((int64_t)p * a.B + b) * nb * kVBlk;
-      D* bmj = reinterpret_cast<D*>(w.bm) + ((int64_t)p * a.B + b) * nb;
-      const int blk = blk0 + lane;
-      block_masks<T>(s_row[warp] + 32 * lane, ilo - (blk << 5), ihi - (blk << 5), mk + (blk << 5), bmj + blk);
+    // masks + minimum of the warp's blocks of row j
+    const int p = j & 1;
+    uint32_t* mk = w.mask + ((int64_t)p * a.B + b) * nb * kVBlk;
+    D* bmj = reinterpret_cast<D*>(w.bm) + ((int64_t)p * a.B + b) * nb;
+#pragma unroll
+    for (int r = 0; r < kK8LRun; ++r) {
+      const int blk = blk0 + r;
+      if (blk <= (ihi >> 5))
+        block_masks_warp<T>(s_row[warp] + 32 * r, ilo - (blk << 5), ihi - (blk << 5), mk + (blk << 5), bmj + blk, lane);
     }
     // descents v[t] > v[t+1] inside the warp's run (pairs across warps: the last CTA)
 #pragma unroll
@@ -639,17 +665,16 @@ __global__ void __launch_bounds__(32 * kK8LWarps, 4) k8l_layer(SolveArgs a, int 
   myd = __reduce_max_sync(0xffffffffu, myd);
   __syncthreads();   // (s_dl initialised)
   if (lane == 0 && myd >= 0) atomicMax(&s_dl, myd);
-  __threadfence();   // this thread's row / mask / minimum stores before the completion count
-  __syncthreads();
+  __syncthreads();   // every thread's row / mask / minimum stores precede thread 0's fence
   if (tid == 0) {
     if (s_dl >= 0) atomicMax(w.dlrun + (int64_t)(j & 1) * a.B + b, s_dl);
-    __threadfence();
+    __threadfence();   // (release: the CTA's stores, ordered by the barrier, before the count)
     s_last = atomicAdd(w.done + b, 1u) == gridDim.x - 1;
+    if (s_last) __threadfence();   // (acquire: the other CTAs' stores before the reads below)
     s_dl = -1;
   }
   __syncthreads();
   if (!s_last) return;
-  __threadfence();
   k8l_row_extras<T>(a, j, w, b, tid, 32 * kK8LWarps, &s_dl);
 }
 
