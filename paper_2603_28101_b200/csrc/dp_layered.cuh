@@ -844,11 +844,11 @@ __global__ void __launch_bounds__(kK3Threads, sizeof(typename Tr<DT, SR>::D) == 
       if (!pa.static_sched) next = atomicAdd(pa.counter, 1ull);
       fetch_meta((int64_t)next);
     }
-    __threadfence();
-    __syncthreads();
+    __syncthreads();   // the CTA's row stores precede thread 0's fence (release, cumulative)
     const int64_t bidx = ((int64_t)j * B + b) * ncb + blk;
     if (!pa.peer_dp) {   // single GPU: count the chunk; consumers wait for the block's chunk count
       if (tid == 0) {
+        __threadfence();
         atomicAdd(pa.ready + bidx, 1ull);
         if (tr) tr[5] = gtimer();
         s_tile = (int64_t)next;
@@ -856,12 +856,13 @@ __global__ void __launch_bounds__(kK3Threads, sizeof(typename Tr<DT, SR>::D) == 
       continue;
     }
     if (tid == 0) {
+      __threadfence();
       s_flag = atomicAdd(pa.blk_done + bidx, 1u) == (unsigned)(nch - 1);
+      if (s_flag) __threadfence();   // (acquire: the block's other chunks)
       if (s_flag && pa.peer_dp) s_flag = wait_flag(pa.start_flag, pa.wait_start, pa.err) ? 1 : 2;
     }
     __syncthreads();
     if (s_flag) {
-      __threadfence();
       if (pa.peer_dp && s_flag == 1) {
         const int64_t roff = ((int64_t)b * (m + 1) + j) * (n + 1);
         const D* mine = reinterpret_cast<const D*>(a.dpws) + roff;
@@ -883,15 +884,16 @@ __global__ void __launch_bounds__(kK3Threads, sizeof(typename Tr<DT, SR>::D) == 
           for (int r = 0; r < pa.own_world; ++r)
             if (r != pa.own_rank) reinterpret_cast<D*>(pa.peer_dp[r])[roff + e] = x;
         }
-        __threadfence_system();
-        __syncthreads();
-        if (tid == 0)
+        __syncthreads();   // every thread's peer stores precede thread 0's system fence
+        if (tid == 0) {
+          __threadfence_system();
           for (int r = 0; r < pa.own_world; ++r)
             if (r != pa.own_rank) {
               atomicAdd_system(pa.peer_ready[r] + bidx, 1ull);
               __threadfence_system();   // the ready increment is visible before the arrival count
               atomicAdd_system(pa.peer_arrive[r], 1ull);   // total, for the end-of-solve barrier
             }
+        }
       }
       if (tid == 0) atomicAdd_system(pa.ready + bidx, 1ull);   // local consumers
     }
