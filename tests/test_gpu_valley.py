@@ -132,6 +132,44 @@ def test_valley_layered_batched_mixed_degrees():
         assert np.array_equal(gpu["bounds"], bounds), batch.name
 
 
+def test_valley_layered_cuda_graph_replay():
+    """K8L's layer launches carry the programmatic-dependent-launch attribute: captured into a
+    CUDA graph (programmatic edges) and replayed, on fresh inputs written into the captured
+    buffers, the results equal an eager solve of the same inputs."""
+    from paper_2603_28101_b200.placer import Placer
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(5)
+    n, m = 4096, 24
+    deg = wl.sorted_degree_vectors(rng, 2, m)
+    mk = lambda: np.stack([wl.presort(wl.predicted(rng, wl.search_lengths(rng, n // 8, 8))) for _ in range(2)]
+                          ).astype(np.float32)
+    pl = Placer.from_profile(wl.float_profile(), max_n=n, max_m=m, max_batch=2, device=0, kernel="layered",
+                             algo="valley")
+    L = torch.from_numpy(mk()).to(dev)
+    D = torch.from_numpy(deg.astype(np.int32)).to(dev)
+    side = torch.cuda.Stream(dev)
+    side.wait_stream(torch.cuda.current_stream(dev))
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(side):
+        pl.solve(L, D)
+        pl.backtrack()
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=side):
+            obj_g, _ = pl.solve(L, D)
+            bnd_g = pl.backtrack()
+    torch.cuda.synchronize()
+    for _ in range(2):
+        L.copy_(torch.from_numpy(mk()))
+        g.replay()
+        torch.cuda.synchronize()
+        got_obj, got_bnd = obj_g.clone(), bnd_g.clone()
+        obj, _ = pl.solve(L, D)
+        bnd = pl.backtrack()
+        torch.cuda.synchronize()
+        assert torch.equal(got_obj, obj) and torch.equal(got_bnd, bnd)
+    pl.close()
+
+
 def test_valley_full_launches_equal_scan(vscan):
     """The bench launches: all 16384 batched problems and the n = 65536, m = 256 instance --
     valley objectives and boundaries identical to the full scan's, problem by problem, and
