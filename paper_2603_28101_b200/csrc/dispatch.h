@@ -38,5 +38,6 @@ K4QFn k4q_for(int dt, int sr, bool kv, bool w);
 K3Fn k3_for(int dt, int sr, bool kp, bool kv, bool w = false);                    // inst_k35.cu
 KPro pro_for(int dt, int sr, bool kp, bool kv);
 K5Fn k5_for(int dt, int sr);
+K8Fn k8c_for(int dt, bool kv, bool w, int v);                       // inst_k8.cu: cluster variants (kK8Cluster CTAs)
 K8Fn k8_for(int dt, bool kp, bool kv, bool w, int wide);          // inst_k8.cu (0: 128, 1: 1024, 2: 512 threads)
 K8LFn k8l_for(int dt, bool kp, bool kv, bool w = false);

@@ -851,6 +851,17 @@ heddle_status heddle_place_init(const heddle_place_config* c, heddle_place_ctx**
       }
       x->k8_smem_max = std::min(x->k8_smem_max, x->smem_optin - (int)fa.sharedSizeBytes);
     }
+    for (int v = 0; v < 12; ++v) {
+      const void* fn = reinterpret_cast<const void*>(k8c_for(x->dtype, v & 1, (v >> 1) & 1, v >> 2));
+      cudaFuncAttributes fa{};
+      if (cudaFuncGetAttributes(&fa, fn) != cudaSuccess ||
+          cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               x->smem_optin - (int)fa.sharedSizeBytes) != cudaSuccess) {
+        heddle_place_destroy(x);
+        return HEDDLE_E_CUDA;
+      }
+      x->k8_smem_max = std::min(x->k8_smem_max, x->smem_optin - (int)fa.sharedSizeBytes);
+    }
   }
   *out = x;
   return HEDDLE_OK;
@@ -1019,7 +1030,34 @@ static heddle_status solve_impl(heddle_place_ctx* x, const heddle_place_problem*
         a.fbounds = x->d_fbounds;
         smem_launch = smem2 + (int)tab;
       }
-      k8_for(x->dtype, kp, kv, wt, variant)<<<p->B, nthreads, smem_launch, s>>>(a);
+      // a few problems: a cluster of kK8Cluster CTAs per problem (each computes a quarter of every
+      // layer's states into every CTA's copy of the row over distributed shared memory)
+      const char* cle = std::getenv("HEDDLE_PLACE_K8_CLUSTER");   // 0 off, 1 auto (default), 2 always (tests)
+      const int cl_mode = cle ? std::atoi(cle) : 1;
+      const int states = p->n - p->m + 1;
+      int cv = 0;   // 512 threads x 8 CTAs (measured best on the TP sweep and the §6.2 size)
+      if (const char* e = std::getenv("HEDDLE_PLACE_K8_CLUSTER_V")) cv = std::atoi(e);   // tuning
+      const int csize = cv == 0 ? 2 * kK8Cluster : kK8Cluster;
+      // (rollout-sized layers stay on one CTA: the cluster barrier costs more than it saves there)
+      const bool cluster = cl_mode != 0 && wide_cta && !kp && (states > 640 || cl_mode == 2) &&
+                           (int64_t)p->B * csize <= x->num_sms;
+      if (cluster) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(p->B * csize);
+        cfg.blockDim = dim3(cv == 2 ? 1024 : 512);
+        cfg.dynamicSmemBytes = smem_launch;
+        cfg.stream = s;
+        cudaLaunchAttribute attr{};
+        attr.id = cudaLaunchAttributeClusterDimension;
+        attr.val.clusterDim.x = csize;
+        attr.val.clusterDim.y = 1;
+        attr.val.clusterDim.z = 1;
+        cfg.attrs = &attr;
+        cfg.numAttrs = 1;
+        if (cudaLaunchKernelEx(&cfg, k8c_for(x->dtype, kv, wt, cv), a) != cudaSuccess) return HEDDLE_E_CUDA;
+      } else {
+        k8_for(x->dtype, kp, kv, wt, variant)<<<p->B, nthreads, smem_launch, s>>>(a);
+      }
       x->launches++;
       if (cudaGetLastError() != cudaSuccess) return HEDDLE_E_CUDA;
     }

@@ -32,6 +32,8 @@
 #include <cstdint>
 #include <type_traits>
 
+#include <cooperative_groups.h>
+
 #include "backtrack.cuh"
 #include "dp_batched.cuh"
 
@@ -41,6 +43,7 @@ namespace hp {
 // plentiful; 1024 threads when there are fewer problems than SMs (TP sweeps, single instances)
 constexpr int kK8Threads = 128;
 constexpr int kK8ThreadsWide = 1024;
+constexpr int kK8Cluster = 4;        // CTAs per problem in the cluster variant (few problems)
 constexpr int kK8ThreadsMid = 512;   // few problems of at most ~512 states per layer: no idle warps
 constexpr int kVBlk = 32;        // range-minimum block (one 32-bit mask per element)
 constexpr int kScanPrefix = 96;  // default SolveArgs::vscan: descent prefixes shorter than this are
@@ -289,15 +292,22 @@ struct K8Smem {
 };
 
 // ---------------------------------------------------------------------------- K8: one CTA per problem
-template <int DT, bool KP, bool KV, bool W, int NT>
-__global__ void __launch_bounds__(NT, 1024 / NT) k8_valley(SolveArgs a) {
+// CL > 1: a thread-block cluster of CL CTAs per problem (few problems: the paper's per-call
+// shapes).  Every CTA holds the whole problem and the full dp rows; CTA r computes the r-th part
+// of each layer's states and stores them into its own row and, over distributed shared memory,
+// into the other CTAs' rows; one cluster barrier per layer replaces the CTA barrier.  The range
+// minimum of the previous row is rebuilt by every CTA on its own copy; CTA 0 writes the rows to
+// the workspace and walks the fused backtrack.
+template <int DT, bool KP, bool KV, bool W, int NT, int CL = 1>
+__global__ void __launch_bounds__(NT, CL > 1 ? 1 : 1024 / NT) k8_valley(SolveArgs a) {
   using T = Tr<DT, HEDDLE_MINMAX>;
   using L = typename T::L;
   using G = typename T::G;
   using D = typename T::D;
   using S = typename SpT<DT>::type;
   extern __shared__ __align__(16) unsigned char smem[];
-  const int N = a.n, M = a.m, b = blockIdx.x, tid = threadIdx.x;   // N, M: strides; n, m: this problem's
+  const int N = a.n, M = a.m, b = blockIdx.x / CL, tid = threadIdx.x;   // N, M: strides; n, m: this problem's
+  const int cr = CL > 1 ? (int)cooperative_groups::this_cluster().block_rank() : 0;
   const int n = prob_n(a, b), m = prob_m(a, b);
   const K8Smem<DT> lay(N, M, KV, W);
   L* sL = reinterpret_cast<L*>(smem + lay.lOff);
@@ -326,6 +336,20 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k8_valley(SolveArgs a) {
   for (int j = 1; j <= m; ++j) {
     D* const prev = (j & 1) ? sdp0 : sdp1;
     D* const cur = (j & 1) ? sdp1 : sdp0;
+    D* rcur[CL];   // this layer's row in every CTA of the cluster (rcur[cr] = cur)
+#pragma unroll
+    for (int r = 0; r < CL; ++r) {
+      if constexpr (CL > 1) rcur[r] = cooperative_groups::this_cluster().map_shared_rank(cur, r);
+      else rcur[r] = cur;
+    }
+    auto put = [&](int i, D v) {   // a computed state into every copy of the row
+      cur[i] = v;
+      if constexpr (CL > 1) {
+#pragma unroll
+        for (int r = 0; r < CL; ++r)
+          if (r != cr) rcur[r][i] = v;
+      }
+    };
     const int ilo = (j == 1) ? 1 : (j == m ? n : j);
     const int ihi = (j == 1 || j < m) ? n - m + j : n;   // m == 1: layer 1 is the last (i up to n)
     int dl = -1;            // last descent of row j-1 (-1: non-decreasing)
@@ -385,7 +409,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k8_valley(SolveArgs a) {
       // one warp (lanes over the splits, lowest-index argmin), dealt round-robin over the warps
       const int pre_hi = scan_prefix ? min(dl + 1, ihi) : ilo - 1;
       const int lane = tid & 31;
-      for (int i = ilo + (tid >> 5); i <= pre_hi; i += NT / 32) {
+      for (int i = ilo + cr * (NT / 32) + (tid >> 5); i <= pre_hi; i += CL * (NT / 32)) {
         D best = T::inf();
         int bk = INT_MAX;
         for (int k = j - 1 + lane; k < i; k += 32) {
@@ -400,38 +424,44 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k8_valley(SolveArgs a) {
           if (ov < best || (ov == best && ok < bk)) { best = ov; bk = ok; }
         }
         if (lane == 0) {
-          cur[i] = best;
+          put(i, best);
           if (KP) gpar[(int64_t)j * (n + 1) + i] = (best == T::inf()) ? -1 : bk;
         }
       }
       // the other states: contiguous runs per thread, so each search gallops from the previous k*
-      const int s0 = pre_hi + 1;
-      const int ns = ihi - s0 + 1;
-      const int per = (ns + NT - 1) / NT;
-      const int r0 = s0 + tid * per, r1 = min(ihi, r0 + per - 1);
+      // (with a cluster: the CTA's contiguous part of them)
+      const int pc = (ihi - pre_hi + CL - 1) / CL;
+      const int s0 = pre_hi + 1 + cr * pc;
+      const int ns = min(ihi, s0 + pc - 1) - s0 + 1;
+      const int per = (max(ns, 0) + NT - 1) / NT;
+      const int r0 = s0 + tid * per, r1 = min(s0 + ns - 1, r0 + per - 1);
       int from = j - 1;
       auto run = [&](auto mono) {
         for (int i = r0; i <= r1; ++i) {
           int arg = -1, ks;
           const D v = V.template solve<KP, decltype(mono)::value>(j - 1, i, from, arg, ks);
           from = ks;
-          cur[i] = v;
+          put(i, v);
           if (KP) gpar[(int64_t)j * (n + 1) + i] = arg;
         }
       };
       if (dl < 0) run(std::true_type{}); else run(std::false_type{});   // (uniform per layer)
     }
-    __syncthreads();
+    if constexpr (CL > 1) cooperative_groups::this_cluster().sync();   // every copy of row j complete
+    else __syncthreads();
     // the finished row to the workspace (coalesced) for the backtrack; -1 parents off the region
-    for (int i = tid; i <= n; i += NT) {
-      const bool in = (i >= ilo && i <= ihi);
-      if (in) gdp[(int64_t)j * (n + 1) + i] = cur[i];
-      if (KP && !in) gpar[(int64_t)j * (n + 1) + i] = -1;
-      if (stab && in) stab[(int64_t)j * (n + 1) + i] = cur[i];
+    if (cr == 0) {
+      for (int i = tid; i <= n; i += NT) {
+        const bool in = (i >= ilo && i <= ihi);
+        if (in) gdp[(int64_t)j * (n + 1) + i] = cur[i];
+        if (KP && !in) gpar[(int64_t)j * (n + 1) + i] = -1;
+        if (stab && in) stab[(int64_t)j * (n + 1) + i] = cur[i];
+      }
     }
     // (cur is read as `prev` by layer j+1 and rewritten by layer j+2, after its barriers; the
     //  masks / sparse levels of row j are built by layer j+1 after this layer's last barrier)
   }
+  if (cr != 0) return;   // (the last cluster barrier ended every remote access to this CTA)
   const D obj = ((m & 1) ? sdp1 : sdp0)[n];
   if (tid == 0) {
     const int st = (obj == T::inf()) ? (int)HEDDLE_E_INFEASIBLE : (int)HEDDLE_OK;

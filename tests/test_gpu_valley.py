@@ -43,6 +43,41 @@ def test_valley_random_tiny_exact(dtype, kernel, vscan):
         gpu["placer"].close()
 
 
+@pytest.mark.parametrize("dtype", ["u32", "f32", "f64"])
+def test_valley_cluster_exact(dtype, monkeypatch):
+    """The cluster variant of K8 (8 CTAs per problem exchanging each layer's states over
+    distributed shared memory; chosen automatically for few problems with > 640 states per
+    layer), forced onto tiny problems -- ties, plateaus, caps, kv caps, weights, mixed degrees,
+    infeasible and invalid problems, parts of a layer with no state -- and onto the rollout
+    config: bit-exact against the oracle (F64: within the tolerance, identical to the scan)."""
+    monkeypatch.setenv("HEDDLE_PLACE_K8_CLUSTER", "2")
+    done = 0
+    for s in range(150):
+        batch = wl.tiny_random(s, n_max=24, m_max=7, allow_caps=True, allow_kv=True, allow_weights=s % 3 == 0,
+                               dtype=dtype)
+        gpu = run_gpu(batch, kernel="batched", algo="valley")
+        p = oracle.Problem.from_batch(batch, 0, mode=dtype)
+        if dtype == "f64":
+            scan = run_gpu(batch, kernel="batched")
+            assert gpu["status"][0] == scan["status"][0]
+            if int(scan["status"][0]) == 0:
+                assert gpu["obj"][0] == scan["obj"][0] and np.array_equal(gpu["bounds"], scan["bounds"]), s
+                assert_f64_tolerance(gpu["obj"][0], gpu["bounds"][0], p, "minmax", tag=f"cl-f64-{s}")
+            scan["placer"].close()
+        else:
+            ref = oracle.solve(p, want_tables=True)
+            assert_exact(gpu, 0, ref, batch, dtype, "minmax", tag=f"cl-{dtype}{s}")
+        gpu["placer"].close()
+        done += 1
+    if dtype == "f32":
+        for prob in range(3):
+            batch = wl.config_rollout(problem=prob)
+            gpu = run_gpu(batch, kernel="batched", algo="valley")
+            ref = oracle.solve(oracle.Problem.from_batch(batch, 0, mode="f32"), want_tables=True)
+            assert_exact(gpu, 0, ref, batch, "f32", "minmax", tag=f"cl-rollout{prob}")
+    assert done == 150
+
+
 @pytest.mark.parametrize("kernel", VALLEY_KERNELS)
 def test_valley_random_tiny_f64(kernel):
     for s in range(100):
