@@ -103,6 +103,17 @@ __device__ __forceinline__ int prob_m(const SolveArgs& a, int b) { return a.ms ?
 // problem's dp rows are packed with its own stride n_b + 1 (every kernel addresses them alike)
 __device__ __forceinline__ int prob_n(const SolveArgs& a, int b) { return a.ns ? __ldg(a.ns + b) : a.n; }
 
+// counter increment with release + acquire semantics at GPU scope: the CTA's stores (ordered
+// before it by a CTA barrier) are visible to whoever observes the count, and the thread that
+// observes the final count sees every other CTA's stores (no separate fence.sc)
+__device__ __forceinline__ unsigned atom_add_acq_rel_gpu(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void red_add_release_gpu(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.release.gpu.global.add.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");

@@ -848,17 +848,15 @@ __global__ void __launch_bounds__(kK3Threads, sizeof(typename Tr<DT, SR>::D) == 
     const int64_t bidx = ((int64_t)j * B + b) * ncb + blk;
     if (!pa.peer_dp) {   // single GPU: count the chunk; consumers wait for the block's chunk count
       if (tid == 0) {
-        __threadfence();
-        atomicAdd(pa.ready + bidx, 1ull);
+        red_add_release_gpu(reinterpret_cast<unsigned long long*>(pa.ready + bidx), 1ull);
         if (tr) tr[5] = gtimer();
         s_tile = (int64_t)next;
       }
       continue;
     }
     if (tid == 0) {
-      __threadfence();
-      s_flag = atomicAdd(pa.blk_done + bidx, 1u) == (unsigned)(nch - 1);
-      if (s_flag) __threadfence();   // (acquire: the block's other chunks)
+      // release (this chunk's stores, ordered by the barrier) + acquire (the block's other chunks)
+      s_flag = atom_add_acq_rel_gpu(pa.blk_done + bidx, 1u) == (unsigned)(nch - 1);
       if (s_flag && pa.peer_dp) s_flag = wait_flag(pa.start_flag, pa.wait_start, pa.err) ? 1 : 2;
     }
     __syncthreads();

@@ -698,9 +698,8 @@ __global__ void __launch_bounds__(32 * kK8LWarps, DT == HEDDLE_F64 ? 2 : 4) k8l_
   __syncthreads();   // every thread's row / mask / minimum stores precede thread 0's fence
   if (tid == 0) {
     if (s_dl >= 0) atomicMax(w.dlrun + (int64_t)(j & 1) * a.B + b, s_dl);
-    __threadfence();   // (release: the CTA's stores, ordered by the barrier, before the count)
-    s_last = atomicAdd(w.done + b, 1u) == gridDim.x - 1;
-    if (s_last) __threadfence();   // (acquire: the other CTAs' stores before the reads below)
+    // release (the CTA's stores, ordered by the barrier) + acquire (the other CTAs' stores)
+    s_last = atom_add_acq_rel_gpu(w.done + b, 1u) == gridDim.x - 1;
     s_dl = -1;
   }
   __syncthreads();
