@@ -697,6 +697,7 @@ void heddle_place_destroy(heddle_place_ctx* ctx) {
   cudaFree(ctx->vws.dlast);
   cudaFree(ctx->vws.dlrun);
   cudaFree(ctx->vws.done);
+  cudaFree(ctx->vws.khint);
   if (ctx->h_epoch) cudaFreeHost(ctx->h_epoch);
   cudaFree(ctx->d_klo);
   cudaFree(ctx->d_wp);
@@ -882,20 +883,22 @@ heddle_status solve_valley_layered(heddle_place_ctx* x, SolveArgs& a, bool kp, b
     const int nbm = vblocks(x->max_n), lvm = vlevels(nbm);
     const size_t des = dp_elem_size(x->dtype, x->semiring);
     void* mk = nullptr;
-    void *bm = nullptr, *sp = nullptr, *smd = nullptr, *dl = nullptr, *dr = nullptr, *dn = nullptr;
+    void *bm = nullptr, *sp = nullptr, *smd = nullptr, *dl = nullptr, *dr = nullptr, *dn = nullptr, *kh = nullptr;
     if (cudaMalloc(&mk, 4 * 2 * (size_t)x->max_batch * nbm * kVBlk) != cudaSuccess ||
         cudaMalloc(&bm, des * 2 * (size_t)x->max_batch * nbm) != cudaSuccess ||
         cudaMalloc(&sp, des * (size_t)x->max_batch * std::max(1, lvm - 1) * nbm) != cudaSuccess ||
         cudaMalloc(&smd, des * (size_t)x->max_batch * (x->max_n + 1)) != cudaSuccess ||
         cudaMalloc(&dl, 4 * (size_t)x->max_batch) != cudaSuccess ||
         cudaMalloc(&dr, 4 * 2 * (size_t)x->max_batch) != cudaSuccess ||
-        cudaMalloc(&dn, 4 * (size_t)x->max_batch) != cudaSuccess) {
+        cudaMalloc(&dn, 4 * (size_t)x->max_batch) != cudaSuccess ||
+        cudaMalloc(&kh, 4 * 2 * (size_t)x->max_batch * (x->max_n + 1)) != cudaSuccess ||
+        cudaMemsetAsync(kh, 0xFF, 4 * 2 * (size_t)x->max_batch * (x->max_n + 1), s) != cudaSuccess) {
       cudaGetLastError();
-      for (void* q : {mk, bm, sp, smd, dl, dr, dn}) cudaFree(q);
+      for (void* q : {mk, bm, sp, smd, dl, dr, dn, kh}) cudaFree(q);
       return HEDDLE_E_NOMEM;
     }
     x->vws = ValleyWs{static_cast<uint32_t*>(mk), bm, sp, smd, static_cast<int*>(dl), static_cast<int*>(dr),
-                      static_cast<unsigned*>(dn), nbm, lvm};
+                      static_cast<unsigned*>(dn), static_cast<int*>(kh), nbm, lvm, x->max_n};
   }
   // per solve: no in-run descents yet, no finished CTAs (the last CTA of each layer resets both)
   if (cudaMemsetAsync(x->vws.dlrun, 0xFF, 4 * 2 * (size_t)B, s) != cudaSuccess ||

@@ -183,7 +183,9 @@ struct Valley {   // ROWPAD: `grow` is the worker's row staged for every size 0.
   // KARY > 2: wide intervals take KARY - 1 independent probes per step (a chain of log_KARY
   // dependent loads instead of log_2: for K8L, whose probes are L2 round trips)
   template <bool ARG, bool MONO = false, int KARY = 2>
-  __device__ __forceinline__ D solve(int lo, int i, int from, int& arg, int& kstar) const {
+  // hint >= lo: a guess of the crossing (K8L: the same state's crossing in the previous layer);
+  // the search gallops from it in the direction the first probe shows, then bisects the bracket
+  __device__ __forceinline__ D solve(int lo, int i, int from, int& arg, int& kstar, int hint = -1) const {
     const int hi = i - 1;
     auto R = [&](int k, int e) -> D {
       if constexpr (MONO) return rm.v[k];
@@ -206,6 +208,27 @@ struct Valley {   // ROWPAD: `grow` is the worker's row staged for every size 0.
         if (crossed(p)) { t = p; break; }
         f = p;
         have_cf = true;
+      }
+    } else if (hint >= lo && hint <= hi) {
+      if (crossed(hint)) {       // the crossing is at or below the hint: gallop down
+        t = hint;
+        for (int step = 1;; step <<= 1) {
+          const int p = t - step;
+          if (p <= f) break;
+          if (crossed(p)) { t = p; continue; }
+          f = p;
+          have_cf = true;
+          break;
+        }
+      } else {                   // above the hint: gallop up
+        f = hint;
+        have_cf = true;
+        for (int step = 1;; step <<= 1) {
+          const int p = f + step;
+          if (p >= t) break;
+          if (crossed(p)) { t = p; break; }
+          f = p;
+        }
       }
     }                            // else: plain bisection of [lo, hi]
     bool have_rt = t <= hi;
@@ -540,7 +563,8 @@ struct ValleyWs {                // K8L range-minimum workspace (per problem, ro
   int* dlast;                    // [B]               last descent of the row (-1: none)
   int* dlrun;                    // [2][B]            descents inside the warps' runs (-1; by parity)
   unsigned* done;                // [B]               CTAs of the current layer finished
-  int nbmax, lvmax;
+  int* khint;                    // [2][B][max_n+1]   each state's crossing in the last two layers
+  int nbmax, lvmax, nmax;
 };
 
 // Row j's range-minimum extras, by the last CTA of layer j to finish (`nt` threads): the last
@@ -625,24 +649,28 @@ __global__ void __launch_bounds__(32 * kK8LWarps, DT == HEDDLE_F64 ? 2 : 4) k8l_
   // launched with programmatic stream serialisation: wait until the previous layer's grid has
   // completed and its stores are visible (the next layer's grid is released after the states)
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (a.status[b] != HEDDLE_OK) return;   // (uniform over the problem's CTAs)
   const int ilo = (j == 1) ? 1 : (j == m ? n : j);
   const int ihi = (j == 1 || j < m) ? n - m + j : n;
   const int blk0 = (ilo >> 5) + kK8LRun * (blockIdx.x * kK8LWarps + warp);
   const bool active = (blk0 << 5) <= ihi;
+  const int x0 = (blk0 << 5) + kK8LRun * lane;
+  // the per-launch loads issued together (one round trip, not one after another)
+  const int status = a.status[b];
+  const int2 rc = a.rowcap[(int64_t)b * m + j - 1];   // {profile row, cap} from the prologue
+  const int dlast = j > 1 ? w.dlast[b] : -1;
+  const int64_t par = (int64_t)a.B * (w.nmax + 1);   // parity stride of the crossing hints
+  const int hint0 = (j > 1 && active && x0 <= n) ? w.khint[((j - 1) & 1) * par + (int64_t)b * (w.nmax + 1) + x0] : -1;
+  if (status != HEDDLE_OK) return;   // (uniform over the problem's CTAs)
   if (tid == 0) s_dl = -1;
   const int nb = vblocks(n);
   D* gdp = reinterpret_cast<D*>(a.dpws) + (int64_t)b * (m + 1) * (n + 1);
-  const int x0 = (blk0 << 5) + kK8LRun * lane;
   if (active) {
-    const int2 rc = a.rowcap[(int64_t)b * m + j - 1];   // {profile row, cap} from the prologue
     const int row = rc.x, cap = rc.y;
     const int pp = (j - 1) & 1;
     const RowMin<T> rm{gdp + (int64_t)(j - 1) * (n + 1), reinterpret_cast<const D*>(w.smd) + (int64_t)b * (n + 1),
                        w.mask + ((int64_t)pp * a.B + b) * nb * kVBlk,
                        reinterpret_cast<const D*>(w.bm) + ((int64_t)pp * a.B + b) * nb,
-                       reinterpret_cast<const D*>(w.sp) + (int64_t)b * (w.lvmax - 1) * nb, nb,
-                       j > 1 ? w.dlast[b] : -1};
+                       reinterpret_cast<const D*>(w.sp) + (int64_t)b * (w.lvmax - 1) * nb, nb, dlast};
     Valley<DT, KV, W> V{reinterpret_cast<const L*>(a.lengths) + (int64_t)b * a.ls, rm,
                         reinterpret_cast<const G*>(a.gtab) + (int64_t)row * a.gstride,
                         KV ? reinterpret_cast<const S*>(a.spws) + (int64_t)b * (n + 1) : nullptr,
@@ -656,13 +684,19 @@ __global__ void __launch_bounds__(32 * kK8LWarps, DT == HEDDLE_F64 ? 2 : 4) k8l_
       D v = T::inf();
       if (i >= ilo && i <= ihi) {
         int arg = -1, ks = from;
+        int* kh = w.khint + (int64_t)b * (w.nmax + 1) + i;
         if (j == 1) {
           v = V.cost(0, i);
           arg = (v == T::inf()) ? -1 : 0;
+          kh[par] = -1;   // (layer 1 has no crossing: layer 2 bisects)
         } else {
-          v = rm.dlast < 0 ? V.template solve<KP, true, kK8LKary>(j - 1, i, from, arg, ks)   // monotone row j-1
-                           : V.template solve<KP, false, kK8LKary>(j - 1, i, from, arg, ks);
+          // the same state's crossing one layer up: usually a few splits away (K8L is bound by the
+          // chain of L2 round trips of this search, not by its instructions)
+          const int hint = (r == 0) ? hint0 : -1;
+          v = rm.dlast < 0 ? V.template solve<KP, true, kK8LKary>(j - 1, i, from, arg, ks, hint)   // monotone row j-1
+                           : V.template solve<KP, false, kK8LKary>(j - 1, i, from, arg, ks, hint);
           from = ks;
+          kh[(j & 1) * par] = ks;
         }
         gdp[(int64_t)j * (n + 1) + i] = v;
         if (KP) a.parws[((int64_t)b * (m + 1) + j) * (n + 1) + i] = arg;
