@@ -46,7 +46,7 @@ constexpr int kK8ThreadsWide = 1024;
 constexpr int kK8Cluster = 4;        // CTAs per problem in the cluster variant (few problems)
 constexpr int kK8ThreadsMid = 512;   // few problems of at most ~512 states per layer: no idle warps
 constexpr int kVBlk = 32;        // range-minimum block (one 32-bit mask per element)
-constexpr int kScanPrefix = 96;  // default SolveArgs::vscan: descent prefixes shorter than this are
+constexpr int kScanPrefix = 64;  // default SolveArgs::vscan: descent prefixes shorter than this are
                                  // scanned state by state (no masks / sparse table built)
 
 __host__ __device__ inline int vblocks(int n) { return (n >> 5) + 1; }          // blocks over indices 0..n

@@ -21,7 +21,7 @@ def _build():
     __graft_entry__.build()
 
 
-@pytest.fixture(params=["96", "0"], ids=["scan-prefix", "masks"])
+@pytest.fixture(params=["64", "0"], ids=["scan-prefix", "masks"])
 def vscan(request, monkeypatch):
     """K8's two descent-prefix paths: scan the few states before the last descent (default), or
     the masks + sparse-table range minimum (HEDDLE_PLACE_VALLEY_SCAN=0)."""
