@@ -652,19 +652,21 @@ __device__ __forceinline__ void bulk_span_out(int lo, int len, int ghi, int& t0,
 __device__ __forceinline__ bool wait_flags_warp(const unsigned long long* flag, unsigned long long target, bool sys,
                                                 int* err) {
   unsigned long long t0 = gtimer();
-  for (;;) {
+  for (unsigned it = 0;; ++it) {
     unsigned long long v = ~0ull;
     if (target) {
       if (sys) asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
       else asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
     }
     if (__all_sync(0xffffffffu, v >= target)) return true;
-    const bool late = gtimer() - t0 > 10000000000ull || *(volatile int*)err;
-    if (__any_sync(0xffffffffu, late)) {
-      if ((threadIdx.x & 31) == 0) atomicExch(err, 1);
-      return false;
+    if ((it & 63) == 63) {   // the timeout / error word every 64 polls: one load per poll otherwise
+      const bool late = gtimer() - t0 > 10000000000ull || *(volatile int*)err;
+      if (__any_sync(0xffffffffu, late)) {
+        if ((threadIdx.x & 31) == 0) atomicExch(err, 1);
+        return false;
+      }
     }
-    __nanosleep(64);
+    __nanosleep(32);
   }
 }
 
