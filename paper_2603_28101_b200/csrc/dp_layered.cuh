@@ -697,7 +697,7 @@ __global__ void __launch_bounds__(kK3Threads, sizeof(typename Tr<DT, SR>::D) == 
   __shared__ int s_valid;
   uint32_t mphase = 0;
   const int64_t ntiles = pa.nentries * B;
-  auto fetch_meta = [&](int64_t t) {   // thread 0
+  auto fetch_meta = [&](int64_t t) {   // one thread
     if (t >= ntiles) return;
     const int4 q = pa.tiles[t / B];
     const int bb = (int)(t % B);
@@ -842,9 +842,12 @@ __global__ void __launch_bounds__(kK3Threads, sizeof(typename Tr<DT, SR>::D) == 
     // (Dequeuing it at the start of the current tile was measured 4 % slower on configs[4]: a
     // ready tile on the dependency chain could sit reserved behind a CTA's long current tile.)
     if (tr && tid == 0) tr[4] = gtimer();
-    if (tid == 0) {
+    // the next tile's dequeue and metadata round trips (thread 32) run beside thread 0's release
+    // of this one (the CTA has already read s_tile and the metadata of this tile)
+    if (tid == 32) {
       if (!pa.static_sched) next = atomicAdd(pa.counter, 1ull);
       fetch_meta((int64_t)next);
+      s_tile = (int64_t)next;
     }
     __syncthreads();   // the CTA's row stores precede thread 0's fence (release, cumulative)
     const int64_t bidx = ((int64_t)j * B + b) * ncb + blk;
@@ -852,7 +855,6 @@ __global__ void __launch_bounds__(kK3Threads, sizeof(typename Tr<DT, SR>::D) == 
       if (tid == 0) {
         red_add_release_gpu(reinterpret_cast<unsigned long long*>(pa.ready + bidx), 1ull);
         if (tr) tr[5] = gtimer();
-        s_tile = (int64_t)next;
       }
       continue;
     }
@@ -897,10 +899,7 @@ __global__ void __launch_bounds__(kK3Threads, sizeof(typename Tr<DT, SR>::D) == 
       }
       if (tid == 0) atomicAdd_system(pa.ready + bidx, 1ull);   // local consumers
     }
-    if (tid == 0) {
-      if (tr) tr[5] = gtimer();
-      s_tile = (int64_t)next;
-    }
+    if (tid == 0 && tr) tr[5] = gtimer();
   }
 }
 
